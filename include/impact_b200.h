@@ -1,0 +1,227 @@
+/*
+ * impact_b200.h -- C-ABI of the B200 IMDP construction + interval-iteration
+ * library (libimpact_b200.so).
+ *
+ * The reference (arxiv 2401.03555's Python package `impact`) has no FFI; its
+ * boundary for this path is the module-level Python API
+ * (pkg/src/impact/__init__.py:4-17).  Each entry point below is what that
+ * API's hot calls bind to; INTEGRATION.md shows the ctypes stubs a maintainer
+ * would add to the reference.  Plain pointers and sizes only, no torch types.
+ *
+ * Conventions
+ *   - every function returns an imp_status; imp_last_error() gives the
+ *     message of the calling thread's last failure (plus row / iteration
+ *     counts where meaningful);
+ *   - row r = (k * n_u + j) * n_w + i  (reference abstraction.py:79-85);
+ *   - columns 0..n_s-1 are safe states, virtual slot n_s is the target
+ *     (r_min/r_max) and n_s+1 the avoid mass (a_min/a_max)
+ *     (reference synthesis.py:79-83);
+ *   - all probabilities / values are IEEE float64;
+ *   - an imp_imdp owns its device memory (one GPU, one shard of rows);
+ *   - one in-flight call per handle; handles are not shared across threads.
+ */
+#ifndef IMPACT_B200_H
+#define IMPACT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum imp_status {
+  IMP_OK = 0,
+  IMP_E_ARG = 1,          /* -> ValueError                                  */
+  IMP_E_CUDA = 2,         /* -> RuntimeError                                */
+  IMP_E_ABSTRACTION = 3,  /* -> AbstractionError (row sums, validate)       */
+  IMP_E_NONFINITE = 4,    /* -> AbstractionError("non-finite objective ...") */
+  IMP_E_CONVERGENCE = 5,  /* -> ConvergenceError(k0, k1)                    */
+  IMP_E_MONOTONE = 6,     /* -> ImpactError (iterates lost monotonicity)    */
+  IMP_E_BRACKET = 7,      /* -> ImpactError (v0 > v1 + 1e-9)                */
+  IMP_E_JIT = 8,          /* -> RuntimeError (NVRTC / module load)          */
+  IMP_E_NOMEM = 9         /* -> MemoryError                                 */
+} imp_status;
+
+typedef struct imp_imdp imp_imdp;
+
+/* Message of the calling thread's last failure; returns its full length. */
+size_t imp_last_error(char* buf, size_t len);
+
+/* Library / device facts: SM count, compute capability, library version. */
+int imp_device_query(int device, int* sm_count, int* cc_major, int* cc_minor);
+const char* imp_version(void);
+
+/* ---------------------------------------------------------------------- */
+/* Abstraction handles                                                     */
+/* ---------------------------------------------------------------------- */
+
+typedef struct imp_imdp_info {
+  int64_t n_rows;      /* rows held by this handle (its shard)             */
+  int64_t row_begin;   /* global index of the first row                    */
+  int64_t nnz;         /* stored t entries (cutoff-sparse)                 */
+  int32_t n_s, n_u, n_w;
+  int32_t k_begin;     /* first safe state of the shard                     */
+  int32_t k_count;     /* safe states in the shard                          */
+  int32_t max_row;     /* longest stored row                                */
+  int32_t device;
+} imp_imdp_info;
+
+/*
+ * Import a cutoff-sparse abstraction shard (CSR over the t columns plus the
+ * r/a vectors) from HOST memory.  Replaces constructing
+ * impact.abstraction.Imdp(...) (reference abstraction.py:88-137) from
+ * arrays, e.g. after impact.fileio.load_abstraction (fileio.py:303-328).
+ * row_ptr has n_rows+1 entries (row_ptr[0] == 0); columns must be
+ * ascending within a row.  The shard covers safe states
+ * [k_begin, k_begin + n_rows / (n_u*n_w)).
+ */
+int imp_imdp_import(int device, int32_t n_s, int32_t n_u, int32_t n_w,
+                    int32_t k_begin, int64_t n_rows, const int64_t* row_ptr,
+                    const int32_t* col, const double* t_lo,
+                    const double* t_hi, const double* r_min,
+                    const double* r_max, const double* a_min,
+                    const double* a_max, imp_imdp** out);
+
+int imp_imdp_info_get(const imp_imdp* h, imp_imdp_info* out);
+
+/* Copy the shard back to HOST memory (row_ptr: n_rows+1, col/t_lo/t_hi:
+ * nnz, vectors: n_rows).  Any pointer may be NULL to skip that array.
+ * Lazy materialisation for fileio / tests (reference Imdp fields). */
+int imp_imdp_export(const imp_imdp* h, int64_t* row_ptr, int32_t* col,
+                    double* t_lo, double* t_hi, double* r_min, double* r_max,
+                    double* a_min, double* a_max);
+
+/* Row-sum / interval invariants of Imdp.validate (abstraction.py:121-137),
+ * evaluated on the device.  Returns IMP_E_ABSTRACTION with the first bad
+ * row in the message. */
+int imp_imdp_validate(const imp_imdp* h, double tol);
+
+void imp_imdp_free(imp_imdp* h);
+
+/* ---------------------------------------------------------------------- */
+/* Construction (reference build_abstraction, abstraction.py:551-599)      */
+/* ---------------------------------------------------------------------- */
+
+typedef struct imp_build_desc {
+  int32_t device;
+  int32_t n, m, p;           /* state / input / disturbance dimensions     */
+  int32_t n_u, n_w;          /* input / disturbance lattice sizes           */
+  int32_t separable;         /* DynamicsSpec.is_separable()                 */
+  /* host geometry, computed with the reference's float64 formulas */
+  const int32_t* counts;     /* (n) lattice points per dimension            */
+  const double* eta;         /* (n)                                         */
+  const double* sigma;       /* (n) diagonal noise                          */
+  const double* edges;       /* (sum(counts)+n) cell edges, dim-major       */
+  const double* cover_lo;    /* (n) [lb - eta/2]                            */
+  const double* cover_hi;    /* (n) [ub + eta/2]                            */
+  int32_t n_s, n_t, n_a;     /* safe / target / avoid counts                */
+  const int32_t* safe_multi;   /* (n_s, n) lattice indices                  */
+  const int32_t* target_multi; /* (n_t, n)                                  */
+  const int32_t* avoid_multi;  /* (n_a, n)                                  */
+  const double* src_lo;      /* (n_s, n) clipped source cells               */
+  const double* src_hi;      /* (n_s, n)                                    */
+  /* dynamics: CUDA source of imp_f<d>(x, k) (expr.lower_dynamics) and the
+   * per-(j,i) folded constants */
+  const char* dyn_source;
+  int32_t n_consts;
+  const double* consts;      /* (n_u*n_w, n_consts)                         */
+  const int32_t* deps;       /* (n, n) dependency lists, -1 padded          */
+  const int32_t* n_deps;     /* (n)                                         */
+  /* AbstractionOptions */
+  double zero_cutoff;
+  double tol;
+  int32_t low_cost;
+  int32_t max_evals_per_dim; /* 0: 200*dim (default); < 0: fixed -v evals   */
+  int32_t multistart;        /* 0 -> 1 + 2*dim                              */
+  /* shard: safe states [k_begin, k_begin + k_count) */
+  int32_t k_begin, k_count;
+} imp_build_desc;
+
+/* Per-build timings (device milliseconds, CUDA events) and counters. */
+typedef struct imp_build_stats {
+  double ms_total, ms_mean_ranges, ms_outer, ms_refine, ms_assemble;
+  int64_t nnz;
+  int64_t nm_instances;
+  int64_t nm_evals;          /* objective evaluations (all NM instances)    */
+} imp_build_stats;
+
+int imp_build(const imp_build_desc* desc, imp_imdp** out,
+              imp_build_stats* stats);
+
+/* ---------------------------------------------------------------------- */
+/* Interval iteration (reference synthesis.py:97-361)                      */
+/* ---------------------------------------------------------------------- */
+
+enum { IMP_SPEC_REACH = 0, IMP_SPEC_SAFETY = 1 };
+enum { IMP_LP_MIN = 0, IMP_LP_MAX = 1 };
+enum { IMP_MODE_PHASE = 0, IMP_MODE_DIAGNOSE = 1 };
+
+typedef struct imp_phase_desc {
+  int32_t spec;          /* IMP_SPEC_*: terminal weights [V, 1, 0] / [V, 0, 1] */
+  int32_t lp;            /* IMP_LP_*: feasible-distribution direction        */
+  int32_t u_max;         /* 1: inputs maximise (reach), 0: minimise (safety) */
+  int32_t mode;          /* IMP_MODE_PHASE (_run_phase) or DIAGNOSE          */
+  double eps;
+  int64_t horizon;       /* <= 0: infinite                                   */
+  int64_t max_iterations;
+  const int64_t* fixed_policy; /* host (k_count) or NULL (phase 1)           */
+} imp_phase_desc;
+
+typedef struct imp_phase_out {
+  double* v0;            /* host (n_s) final lower-track values              */
+  double* v1;            /* host (n_s) final upper-track values              */
+  int64_t* policy;       /* host (n_s) or NULL                               */
+  int64_t iterations;
+  int64_t k0, k1;        /* first self-converged iteration, -1 if never      */
+  int32_t fallback;      /* stalled-gap fallback fired                       */
+  double gap;            /* final max(v1 - v0)                               */
+  double ms_device;      /* device time of the loop (CUDA events)            */
+  int64_t sweeps;        /* twin sweeps executed                             */
+} imp_phase_out;
+
+/* Run one synthesis phase to termination (reference _run_phase,
+ * synthesis.py:145-205; diagnose_convergence :321-361 with
+ * IMP_MODE_DIAGNOSE).  Single-shard handles only; the loop, the stable
+ * sorts, the sweeps and the termination logic all run on the device in
+ * CUDA graphs.  IMP_E_CONVERGENCE / _MONOTONE / _BRACKET carry the
+ * reference's error semantics (k0/k1 are filled in either way). */
+int imp_run_phase(imp_imdp* h, const imp_phase_desc* desc,
+                  imp_phase_out* out);
+
+/* One robust Bellman update (reference bellman_step, synthesis.py:97-135)
+ * from host values (n_s) -> new values (k_count) and chosen inputs. */
+int imp_bellman_step(imp_imdp* h, const double* values, int32_t spec,
+                     int32_t lp, int32_t u_max, const int64_t* fixed_policy,
+                     double* new_values, int64_t* chosen);
+
+/* Row-level greedy LP values (reference RowsSolver.values,
+ * feasible.py:96-111) for every stored row: out[r] for weights w (n_s+2).
+ * Device pointers are accepted when on_device != 0. */
+int imp_row_values(imp_imdp* h, const double* weights, int32_t lp,
+                   double* out, int32_t on_device);
+
+/* ---------------------------------------------------------------------- */
+/* Sharded iteration (multi-GPU): the host exchanges V between sweeps.     */
+/* ---------------------------------------------------------------------- */
+
+/* One twin sweep of this shard against the full value vectors v0/v1
+ * (device pointers, n_s each): writes this shard's new values to
+ * new0/new1 (device, k_count each), chosen inputs to policy (device,
+ * k_count) and the shard's max |dV0|, max |dV1|, max(v1'-v0') and the
+ * monotone/bracket flags to stats[0..4] (device doubles).  stream is a
+ * cudaStream_t (NULL = legacy default). */
+int imp_shard_sweep(imp_imdp* h, const double* v0, const double* v1,
+                    int32_t spec, int32_t lp, int32_t u_max,
+                    const int64_t* fixed_policy_dev, double* new0,
+                    double* new1, int64_t* policy, double* stats,
+                    void* stream);
+
+/* Microbenchmark used for the FP64 roofline denominator: DFMA throughput
+ * (GFLOP/s, 2 flops per DFMA) measured with CUDA events. */
+int imp_fp64_peak(int device, double* gflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IMPACT_B200_H */

@@ -1,0 +1,347 @@
+"""IMDP construction on the B200 (drop-in for pkg/src/impact/abstraction.py).
+
+Public surface kept from the reference: AbstractionOptions (:52-70),
+RowIndex (:73-85), Imdp (:88-137), estimate_cost (:140-157) and
+build_abstraction (:551-599).
+
+What changes underneath: the abstraction lives in HBM as a cutoff-sparse
+CSR (columns with t_min = t_max = 0 are not stored: they carry no lower mass
+and no headroom, so no LP value depends on them), built by the JIT-compiled
+construction kernels of csrc/build.cu.  `Imdp.t_min` / `t_max` are
+materialised lazily on the host only when a caller touches them (fileio,
+tests).  An Imdp constructed from dense host arrays, as the reference's own
+tests do, is uploaded on first use.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import AbstractionError
+from .expr import lower_dynamics
+from .grid import LabeledStates, Space, domain_box, multi_indices
+from .noise import DiagonalNormal
+
+__all__ = ["AbstractionOptions", "RowIndex", "Imdp", "estimate_cost",
+           "build_abstraction", "BuildReport"]
+
+_ROW_SUM_TOL = 1e-9
+
+
+@dataclass(frozen=True)
+class AbstractionOptions:
+    low_cost: bool = False
+    optimizer_max_evals: int = 0      # 0 -> 200 * dim
+    optimizer_tol: float = 1e-8
+    zero_cutoff: float = 1e-12
+    multistart: int = 0               # 0 -> 1 + 2 * dim
+    workers: int = 1                  # accepted for API parity; unused on GPU
+    mc_seed: int = 0
+
+    def __post_init__(self):
+        if not self.zero_cutoff < 1e-6:
+            raise ValueError("zero_cutoff must be < 1e-6")
+
+    def max_evals_for(self, dim):
+        return self.optimizer_max_evals or 200 * max(dim, 1)
+
+    def multistart_for(self, dim):
+        return self.multistart or 1 + 2 * dim
+
+
+@dataclass(frozen=True)
+class RowIndex:
+    """(safe position k, input j, disturbance i) <-> row, state-major."""
+    n_u: int
+    n_w: int
+
+    def row(self, k, j=0, i=0):
+        return (k * self.n_u + j) * self.n_w + i
+
+    def kji(self, row):
+        rest, i = divmod(row, self.n_w)
+        k, j = divmod(rest, self.n_u)
+        return k, j, i
+
+
+def estimate_cost(n_s, n_u=1, n_w=1):
+    """(entries d = rows * n_s, dense bytes, overflow flag)."""
+    n_u = n_u or 1
+    n_w = n_w or 1
+    if min(n_s, n_u, n_w) < 0:
+        raise ValueError("counts must be non-negative")
+    rows = n_s * n_u * n_w
+    d = rows * n_s
+    nbytes = 16 * d + 48 * rows
+    cap = 2**63 - 1
+    return min(d, cap), min(nbytes, cap), d > cap or nbytes > cap
+
+
+class _Handle:
+    """Owner of one imp_imdp* (device memory)."""
+
+    def __init__(self, raw):
+        self.raw = raw
+
+    def __del__(self):
+        if self.raw:
+            try:
+                _lib.load().imp_imdp_free(self.raw)
+            except Exception:
+                pass
+            self.raw = None
+
+    def info(self):
+        out = _lib.ImdpInfo()
+        _lib.check(_lib.load().imp_imdp_info_get(self.raw, ctypes.byref(out)))
+        return out
+
+
+def csr_from_dense(t_min, t_max):
+    """Cutoff-sparse CSR of dense bounds: entries with either bound != 0."""
+    t_min = np.asarray(t_min, dtype=float)
+    t_max = np.asarray(t_max, dtype=float)
+    live = (t_min != 0) | (t_max != 0)
+    counts = live.sum(axis=1)
+    ptr = np.zeros(t_min.shape[0] + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    rows, cols = np.nonzero(live)
+    return ptr, cols.astype(np.int32), t_min[rows, cols], t_max[rows, cols]
+
+
+def import_csr(n_s, n_u, n_w, ptr, col, lo, hi, r_min, r_max, a_min, a_max,
+               k_begin=0, device=0):
+    lib = _lib.load()
+    ptr, col = _lib.as_i64(ptr), _lib.as_i32(col)
+    lo, hi = _lib.as_f64(lo), _lib.as_f64(hi)
+    vecs = [_lib.as_f64(v) for v in (r_min, r_max, a_min, a_max)]
+    raw = ctypes.c_void_p()
+    _lib.check(lib.imp_imdp_import(
+        device, n_s, n_u, n_w, k_begin, len(ptr) - 1,
+        _lib.ptr(ptr, _lib.c_i64), _lib.ptr(col, _lib.c_i32),
+        _lib.ptr(lo, _lib.c_dbl), _lib.ptr(hi, _lib.c_dbl),
+        *[_lib.ptr(v, _lib.c_dbl) for v in vecs], ctypes.byref(raw)))
+    return _Handle(raw)
+
+
+class Imdp:
+    """Interval MDP abstraction (reference abstraction.py:88-137).
+
+    Either constructed like the reference's dataclass from dense host arrays
+    (uploaded on first device use), or returned by build_abstraction with
+    the bounds already resident on the GPU (host arrays materialised on
+    first access).
+    """
+
+    def __init__(self, state_space: Space, input_space, disturb_space,
+                 labels: LabeledStates, t_min=None, t_max=None, r_min=None,
+                 r_max=None, a_min=None, a_max=None, *, _handle=None):
+        self.state_space = state_space
+        self.input_space = input_space
+        self.disturb_space = disturb_space
+        self.labels = labels
+        self._host = {}
+        for k, v in (("t_min", t_min), ("t_max", t_max), ("r_min", r_min),
+                     ("r_max", r_max), ("a_min", a_min), ("a_max", a_max)):
+            if v is not None:
+                self._host[k] = np.asarray(v, dtype=float)
+        self._handle = _handle
+        self.build_report = None
+        if _handle is None and len(self._host) != 6:
+            raise ValueError("Imdp needs all six bound arrays or a device "
+                             "handle")
+
+    # --- reference properties -------------------------------------------
+    @property
+    def n_s(self):
+        return len(self.labels.safe)
+
+    @property
+    def n_u(self):
+        return self.input_space.total if self.input_space is not None else 1
+
+    @property
+    def n_w(self):
+        return self.disturb_space.total if self.disturb_space is not None \
+            else 1
+
+    @property
+    def n_rows(self):
+        return self.n_s * self.n_u * self.n_w
+
+    @property
+    def rows(self):
+        return RowIndex(self.n_u, self.n_w)
+
+    # --- device residency -------------------------------------------------
+    def device_handle(self):
+        """imp_imdp* of this abstraction, uploading host arrays if needed."""
+        if self._handle is None:
+            h = self._host
+            ptr, col, lo, hi = csr_from_dense(h["t_min"], h["t_max"])
+            self._handle = import_csr(self.n_s, self.n_u, self.n_w, ptr, col,
+                                      lo, hi, h["r_min"], h["r_max"],
+                                      h["a_min"], h["a_max"])
+        return self._handle
+
+    def csr(self):
+        """Host copy of the stored shard: (row_ptr, col, lo, hi, r_min,
+        r_max, a_min, a_max)."""
+        hd = self.device_handle()
+        info = hd.info()
+        n, nnz = info.n_rows, info.nnz
+        ptr = np.empty(n + 1, np.int64)
+        col = np.empty(nnz, np.int32)
+        lo = np.empty(nnz)
+        hi = np.empty(nnz)
+        vec = [np.empty(n) for _ in range(4)]
+        _lib.check(_lib.load().imp_imdp_export(
+            hd.raw, _lib.ptr(ptr, _lib.c_i64), _lib.ptr(col, _lib.c_i32),
+            _lib.ptr(lo, _lib.c_dbl), _lib.ptr(hi, _lib.c_dbl),
+            *[_lib.ptr(v, _lib.c_dbl) for v in vec]))
+        return (ptr, col, lo, hi, *vec)
+
+    def _materialise(self):
+        ptr, col, lo, hi, r0, r1, a0, a1 = self.csr()
+        n = len(ptr) - 1
+        t_min = np.zeros((n, self.n_s))
+        t_max = np.zeros((n, self.n_s))
+        rows = np.repeat(np.arange(n), np.diff(ptr))
+        t_min[rows, col] = lo
+        t_max[rows, col] = hi
+        self._host.update(t_min=t_min, t_max=t_max, r_min=r0, r_max=r1,
+                          a_min=a0, a_max=a1)
+
+    def _get(self, key):
+        if key not in self._host:
+            self._materialise()
+        return self._host[key]
+
+    t_min = property(lambda self: self._get("t_min"))
+    t_max = property(lambda self: self._get("t_max"))
+    r_min = property(lambda self: self._get("r_min"))
+    r_max = property(lambda self: self._get("r_max"))
+    a_min = property(lambda self: self._get("a_min"))
+    a_max = property(lambda self: self._get("a_max"))
+
+    @property
+    def nnz(self):
+        return self.device_handle().info().nnz
+
+    def validate(self):
+        """Interval and row-sum invariants (reference :121-137), on device."""
+        _lib.check(_lib.load().imp_imdp_validate(self.device_handle().raw,
+                                                 _ROW_SUM_TOL))
+
+
+@dataclass
+class BuildReport:
+    """Device-side timings and counters of one build_abstraction call."""
+    ms_total: float
+    ms_mean_ranges: float
+    ms_outer: float
+    ms_refine: float
+    ms_assemble: float
+    nnz: int
+    nm_instances: int
+    nm_evals: int
+    rows: int
+    entries: int          # rows * n_s: the reference's `d`
+
+
+def build_abstraction(dyn, noise, spaces, labels, opts=None,
+                      device=0, k_range=None) -> Imdp:
+    """Construct the interval abstraction on the GPU.
+
+    spaces = (state, input or None, disturbance or None), exactly as the
+    reference (abstraction.py:551-599).  `k_range=(k_begin, k_count)`
+    builds one shard of safe states (multi-GPU row sharding); the default
+    is all of them.
+    """
+    opts = opts or AbstractionOptions()
+    state, inp, dist = spaces
+    n, m, p = dyn.dims
+    if state.dim != n:
+        raise AbstractionError("state space dimension mismatch")
+    if m and (inp is None or inp.dim != m):
+        raise AbstractionError("input space dimension mismatch")
+    if p and (dist is None or dist.dim != p):
+        raise AbstractionError("disturbance space dimension mismatch")
+    if not isinstance(noise, DiagonalNormal):
+        raise AbstractionError(
+            "only diagonal Gaussian noise runs on the B200 path (Monte "
+            "Carlo noise models are a later row, SURVEY.md 8(f))")
+    if noise.dim != n:
+        raise AbstractionError("noise dimension mismatch")
+    n_s = len(labels.safe)
+    if n_s < 1:
+        raise AbstractionError("no safe states to abstract")
+    u_reps = inp.rep_points() if inp is not None else np.zeros((1, 0))
+    w_reps = dist.rep_points() if dist is not None else np.zeros((1, 0))
+    n_u, n_w = len(u_reps), len(w_reps)
+    k_begin, k_count = k_range if k_range is not None else (0, n_s)
+
+    lowered = lower_dynamics(dyn, u_reps, w_reps)
+    counts = _lib.as_i32(state.counts)
+    edges = _lib.as_f64(np.concatenate([state.edges(d) for d in range(n)]))
+    cover = domain_box(state)
+    safe_multi = multi_indices(state, labels.safe)
+    # clipped source cells (abstraction.py:231-235)
+    rep = state.lb + safe_multi * state.eta
+    src_lo = _lib.as_f64(np.maximum(rep - state.eta / 2, state.lb))
+    src_hi = _lib.as_f64(np.minimum(rep + state.eta / 2, state.ub))
+    deps = np.full((n, n), -1, dtype=np.int32)
+    n_deps = np.zeros(n, dtype=np.int32)
+    for d, dl in enumerate(lowered.deps):
+        deps[d, :len(dl)] = dl
+        n_deps[d] = len(dl)
+    arrays = dict(
+        counts=counts, eta=_lib.as_f64(state.eta),
+        sigma=_lib.as_f64(noise.sigma), edges=edges,
+        cover_lo=_lib.as_f64(cover.lo), cover_hi=_lib.as_f64(cover.hi),
+        safe_multi=_lib.as_i32(safe_multi),
+        target_multi=_lib.as_i32(multi_indices(state, labels.target)
+                                 .reshape(-1, n)),
+        avoid_multi=_lib.as_i32(multi_indices(state, labels.avoid)
+                                .reshape(-1, n)),
+        src_lo=src_lo, src_hi=src_hi, consts=_lib.as_f64(lowered.consts),
+        deps=_lib.as_i32(deps), n_deps=_lib.as_i32(n_deps))
+    desc = _lib.BuildDesc()
+    desc.device = device
+    desc.n, desc.m, desc.p = n, m, p
+    desc.n_u, desc.n_w = n_u, n_w
+    desc.separable = int(dyn.is_separable())
+    for key in ("counts", "safe_multi", "target_multi", "avoid_multi",
+                "deps", "n_deps"):
+        setattr(desc, key, _lib.ptr(arrays[key], _lib.c_i32))
+    for key in ("eta", "sigma", "edges", "cover_lo", "cover_hi", "src_lo",
+                "src_hi", "consts"):
+        setattr(desc, key, _lib.ptr(arrays[key], _lib.c_dbl))
+    desc.n_s = n_s
+    desc.n_t = len(labels.target)
+    desc.n_a = len(labels.avoid)
+    src = lowered.source.encode()
+    desc.dyn_source = src
+    desc.n_consts = lowered.consts.shape[1]
+    desc.zero_cutoff = opts.zero_cutoff
+    desc.tol = opts.optimizer_tol
+    desc.low_cost = int(opts.low_cost)
+    desc.max_evals_per_dim = 0
+    if opts.optimizer_max_evals:
+        desc.max_evals_per_dim = -int(opts.optimizer_max_evals)
+    desc.multistart = int(opts.multistart)
+    desc.k_begin, desc.k_count = k_begin, k_count
+    raw = ctypes.c_void_p()
+    stats = _lib.BuildStats()
+    _lib.check(_lib.load().imp_build(ctypes.byref(desc), ctypes.byref(raw),
+                                     ctypes.byref(stats)))
+    handle = _Handle(raw)
+    imdp = Imdp(state, inp, dist, labels, _handle=handle)
+    rows = k_count * n_u * n_w
+    imdp.build_report = BuildReport(
+        stats.ms_total, stats.ms_mean_ranges, stats.ms_outer,
+        stats.ms_refine, stats.ms_assemble, stats.nnz, stats.nm_instances,
+        stats.nm_evals, rows, rows * n_s)
+    return imdp
