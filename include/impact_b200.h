@@ -149,6 +149,12 @@ typedef struct imp_build_stats {
 int imp_build(const imp_build_desc* desc, imp_imdp** out,
               imp_build_stats* stats);
 
+/* NVRTC-compile (only) the construction module imp_build would use for
+ * desc's dynamics; no device needed.  Writes the sm_100a cubin to
+ * cubin_path when non-NULL (for cuobjdump).  IMP_E_JIT carries the NVRTC
+ * log in imp_last_error(). */
+int imp_jit_compile(const imp_build_desc* desc, const char* cubin_path);
+
 /* ---------------------------------------------------------------------- */
 /* Interval iteration (reference synthesis.py:97-361)                      */
 /* ---------------------------------------------------------------------- */

@@ -30,20 +30,18 @@ JIT_SOURCES = ["ndtr.h", "jit/construct.cuh"]
 
 
 def _embed_jit():
-    """Write csrc/_jit_source.inc: the JIT kernel source as a C++ raw
-    string (ndtr.h + jit/construct.cuh concatenated)."""
-    parts = []
-    for rel in JIT_SOURCES:
+    """Write csrc/_jit_source.inc: the JIT sources as C++ raw strings
+    (kJitPrelude = ndtr.h, kJitKernels = jit/construct.cuh); the generated
+    config + dynamics go between them at run time."""
+    decls = []
+    for name, rel in zip(("kJitPrelude", "kJitKernels"), JIT_SOURCES):
         with open(os.path.join(CSRC, rel)) as fh:
-            text = fh.read()
-        parts.append(f"// ---- {rel} ----\n" +
-                     text.replace('#include "../ndtr.h"', "")
-                     .replace("#pragma once", ""))
-    body = "\n".join(parts)
+            body = fh.read().replace("#pragma once", "")
+        chunks = [body[i:i + 12000] for i in range(0, len(body), 12000)]
+        lit = "\n".join(f'R"IMPJIT({c})IMPJIT"' for c in chunks)
+        decls.append(f"static const char {name}[] =\n{lit};\n")
     out = os.path.join(CSRC, "_jit_source.inc")
-    chunks = [body[i:i + 12000] for i in range(0, len(body), 12000)]
-    lit = "\n".join(f'R"IMPJIT({c})IMPJIT"' for c in chunks)
-    new = f"static const char kJitSource[] =\n{lit};\n"
+    new = "\n".join(decls)
     old = open(out).read() if os.path.exists(out) else None
     if old != new:
         with open(out, "w") as fh:
@@ -88,8 +86,7 @@ def build(force=False, verbose=False):
             sys.stderr.write(out.decode())
             raise RuntimeError(f"nvcc failed on {unit}")
     link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs,
-            f"-L{CUDA}/lib64", f"-L{CUDA}/lib64/stubs", "-lcudart", "-lnvrtc",
-            "-lcuda", "-Xlinker", f"-rpath,{CUDA}/lib64"]
+            f"-L{CUDA}/lib64", f"-L{CUDA}/lib64/stubs", "-lcudart", "-lnvrtc", "-Xlinker", f"-rpath,{CUDA}/lib64"]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.run(link, check=True)

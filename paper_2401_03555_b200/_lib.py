@@ -100,8 +100,11 @@ def _declare(lib):
     lib.imp_shard_sweep.argtypes = [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32,
                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]
     lib.imp_fp64_peak.argtypes = [c_i32, P_dbl]
+    lib.imp_jit_compile.argtypes = [ctypes.POINTER(BuildDesc),
+                                    ctypes.c_char_p]
     for name in ("imp_device_query", "imp_imdp_import", "imp_imdp_info_get",
                  "imp_imdp_export", "imp_imdp_validate", "imp_build",
+                 "imp_jit_compile",
                  "imp_run_phase", "imp_bellman_step", "imp_row_values",
                  "imp_shard_sweep", "imp_fp64_peak"):
         getattr(lib, name).restype = c_i32
@@ -110,6 +113,7 @@ def _declare(lib):
 EXPORTED = ("imp_last_error", "imp_version", "imp_device_query",
             "imp_imdp_import", "imp_imdp_info_get", "imp_imdp_export",
             "imp_imdp_validate", "imp_imdp_free", "imp_build",
+            "imp_jit_compile",
             "imp_run_phase", "imp_bellman_step", "imp_row_values",
             "imp_shard_sweep", "imp_fp64_peak")
 

@@ -260,6 +260,34 @@ def build_abstraction(dyn, noise, spaces, labels, opts=None,
     builds one shard of safe states (multi-GPU row sharding); the default
     is all of them.
     """
+    state, inp, dist = spaces
+    desc, keep = describe(dyn, noise, spaces, labels, opts, device, k_range)
+    raw = ctypes.c_void_p()
+    stats = _lib.BuildStats()
+    _lib.check(_lib.load().imp_build(ctypes.byref(desc), ctypes.byref(raw),
+                                     ctypes.byref(stats)))
+    del keep
+    handle = _Handle(raw)
+    imdp = Imdp(state, inp, dist, labels, _handle=handle)
+    rows = desc.k_count * desc.n_u * desc.n_w
+    imdp.build_report = BuildReport(
+        stats.ms_total, stats.ms_mean_ranges, stats.ms_outer,
+        stats.ms_refine, stats.ms_assemble, stats.nnz, stats.nm_instances,
+        stats.nm_evals, rows, rows * desc.n_s)
+    return imdp
+
+
+def jit_compile(dyn, noise, spaces, labels, opts=None, cubin_path=None):
+    """NVRTC-compile the construction module for this system (no GPU
+    needed); raises RuntimeError with the NVRTC log on failure."""
+    desc, keep = describe(dyn, noise, spaces, labels, opts, 0, None)
+    path = None if cubin_path is None else str(cubin_path).encode()
+    _lib.check(_lib.load().imp_jit_compile(ctypes.byref(desc), path))
+    del keep
+
+
+def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
+    """imp_build_desc for a system plus the host arrays it points into."""
     opts = opts or AbstractionOptions()
     state, inp, dist = spaces
     n, m, p = dyn.dims
@@ -333,15 +361,4 @@ def build_abstraction(dyn, noise, spaces, labels, opts=None,
         desc.max_evals_per_dim = -int(opts.optimizer_max_evals)
     desc.multistart = int(opts.multistart)
     desc.k_begin, desc.k_count = k_begin, k_count
-    raw = ctypes.c_void_p()
-    stats = _lib.BuildStats()
-    _lib.check(_lib.load().imp_build(ctypes.byref(desc), ctypes.byref(raw),
-                                     ctypes.byref(stats)))
-    handle = _Handle(raw)
-    imdp = Imdp(state, inp, dist, labels, _handle=handle)
-    rows = k_count * n_u * n_w
-    imdp.build_report = BuildReport(
-        stats.ms_total, stats.ms_mean_ranges, stats.ms_outer,
-        stats.ms_refine, stats.ms_assemble, stats.nnz, stats.nm_instances,
-        stats.nm_evals, rows, rows * n_s)
-    return imdp
+    return desc, (arrays, src, lowered)

@@ -1,8 +1,476 @@
-// Construction host driver (placeholder while the JIT kernels land).
+// IMDP construction host driver (reference build_abstraction,
+// pkg/src/impact/abstraction.py:551-599).
+//
+// The construction kernels (jit/construct.cuh) are specialised per dynamics
+// spec with NVRTC: the generated source fixes the state dimension, the
+// dependency structure and the x-dependent residual of every f_d, so the
+// Nelder-Mead objective is straight-line FP64 code with the simplex
+// dimension known at compile time.  Compiled for sm_100a with --fmad=false
+// (numpy's rounding of a*b + c); modules are cached per source in-process.
+//
+// Pipeline on one stream: stage 1 mean ranges -> stage 2 count -> CUB scan
+// -> stage 2 write -> [stage 3 NM refinement, coupled only] -> stage 4
+// assemble -> slack / row stats.  Device time per stage via CUDA events.
+#include <cub/device/device_scan.cuh>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
 #include "common.h"
 #include "_jit_source.inc"
+
+namespace imp {
+namespace {
+
+// Host mirror of BuildParams in jit/construct.cuh (identical layout).
+struct BuildParams {
+  int n_u, n_w, k_begin, k_count;
+  long long n_rows;
+  int n_s, n_t, n_a, total;
+  const int* counts;
+  const int* edge_off;
+  const int* strides;
+  const double* eta;
+  const double* sigma;
+  const double* edges;
+  const double* cover_lo;
+  const double* cover_hi;
+  const double* src_lo;
+  const double* src_hi;
+  const double* consts;
+  const int* label;
+  const int* safe_flat;
+  const int* target_flat;
+  const int* avoid_flat;
+  double cutoff, tol;
+  int low_cost, separable;
+  int max_evals_fixed;
+  int multistart;
+  double* mlo;
+  double* mhi;
+  int write;
+  long long* t_count;
+  long long* x_count;
+  const long long* row_ptr;
+  const long long* aux_ptr;
+  int* col;
+  double* lo;
+  double* hi;
+  int* aux_code;
+  double* aux_min;
+  double* aux_max;
+  double* raw;
+  long long n_items;
+  long long* evals;
+  double* r_min;
+  double* r_max;
+  double* a_min;
+  double* a_max;
+  unsigned long long* err;
+  double* err_val;
+};
+
+// JIT modules go through the runtime's library API (cudaLibrary_t /
+// cudaKernel_t), so libimpact_b200.so never links libcuda directly and
+// loads on hosts without a driver (the CPU build check).
+struct JitModule {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t mean = nullptr, outer = nullptr, refine = nullptr,
+               assemble = nullptr;
+};
+
+std::mutex g_jit_mu;
+std::map<std::string, JitModule> g_jit_cache;
+
+std::string config_header(const imp_build_desc* d) {
+  std::ostringstream o;
+  o << "#define IMP_N " << d->n << "\n#define IMP_NC "
+    << std::max(d->n_consts, 1) << "\n";
+  o << "__device__ constexpr int kNDeps[IMP_N] = {";
+  for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->n_deps[q];
+  o << "};\n__device__ constexpr int kDeps[IMP_N][IMP_N] = {";
+  for (int q = 0; q < d->n; ++q) {
+    o << (q ? ", {" : "{");
+    for (int e = 0; e < d->n; ++e) o << (e ? ", " : "") << d->deps[q * d->n + e];
+    o << "}";
+  }
+  o << "};\n";
+  return o.str();
+}
+
+std::string jit_source(const std::string& dyn_part) {
+  return std::string(kJitPrelude) + "\n" +
+         "__device__ __forceinline__ double imp_min(double, double);\n"
+         "__device__ __forceinline__ double imp_max(double, double);\n" +
+         dyn_part + "\n" + kJitKernels;
+}
+
+// NVRTC: source -> sm_100a cubin (no device needed).
+std::vector<char> compile_cubin(const std::string& src) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "impact_construct.cu", 0,
+                         nullptr, nullptr) != NVRTC_SUCCESS)
+    fail(IMP_E_JIT, "nvrtcCreateProgram failed");
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false",
+                        "-std=c++17", "-lineinfo"};
+  nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    set_error("NVRTC compile of the construction module failed:\n%s",
+              log.c_str());
+    throw Failure{IMP_E_JIT};
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::vector<char> cubin(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+JitModule& jit(int device, const std::string& dyn_part) {
+  const std::string src = jit_source(dyn_part);
+  const std::string key = std::to_string(device) + "\n" + src;
+  std::lock_guard<std::mutex> lk(g_jit_mu);
+  auto it = g_jit_cache.find(key);
+  if (it != g_jit_cache.end()) return it->second;
+  std::vector<char> cubin = compile_cubin(src);
+  IMP_CUDA(cudaSetDevice(device));
+  IMP_CUDA(cudaFree(nullptr));  // bind the primary context
+  JitModule m;
+  IMP_CUDA(cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0,
+                               nullptr, nullptr, 0));
+  IMP_CUDA(cudaLibraryGetKernel(&m.mean, m.lib, "k_mean_ranges"));
+  IMP_CUDA(cudaLibraryGetKernel(&m.outer, m.lib, "k_outer"));
+  IMP_CUDA(cudaLibraryGetKernel(&m.refine, m.lib, "k_refine"));
+  IMP_CUDA(cudaLibraryGetKernel(&m.assemble, m.lib, "k_assemble"));
+  return g_jit_cache.emplace(key, m).first->second;
+}
+
+void launch(cudaKernel_t f, unsigned grid, unsigned block, size_t smem,
+            cudaStream_t s, BuildParams& P) {
+  const void* fn = reinterpret_cast<const void*>(f);
+  if (smem > 48 * 1024)
+    IMP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  void* args[] = {&P};
+  IMP_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, s));
+}
+
+template <class T>
+DevBuf<T> upload(const T* src, size_t n, cudaStream_t s) {
+  DevBuf<T> b(std::max<size_t>(n, 1));
+  if (n) IMP_CUDA(cudaMemcpyAsync(b.ptr, src, n * sizeof(T),
+                                  cudaMemcpyHostToDevice, s));
+  return b;
+}
+
+void exclusive_scan(long long* counts, long long* out, int64_t n,
+                    cudaStream_t s) {
+  size_t bytes = 0;
+  IMP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, out, n, s));
+  DevBuf<unsigned char> tmp(std::max<size_t>(bytes, 16));
+  IMP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, bytes, counts, out, n, s));
+}
+
+struct Events {
+  cudaEvent_t e[6];
+  Events() { for (auto& x : e) cudaEventCreate(&x); }
+  ~Events() { for (auto& x : e) cudaEventDestroy(x); }
+  float ms(int a, int b) {
+    float v = 0.f;
+    cudaEventElapsedTime(&v, e[a], e[b]);
+    return v;
+  }
+};
+
+}  // namespace
+}  // namespace imp
+
 using namespace imp;
+
 extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
                          imp_build_stats* stats) {
-  return guarded([&] { fail(IMP_E_ARG, "imp_build: not implemented yet"); });
+  imp_imdp* h = nullptr;
+  int st = guarded([&] {
+    IMP_REQUIRE(d && out, "null argument");
+    const int N = d->n;
+    IMP_REQUIRE(N >= 1 && N <= 16, "state dimension %d unsupported", N);
+    IMP_REQUIRE(d->n_s >= 1, "no safe states to abstract");
+    IMP_REQUIRE(d->k_begin >= 0 && d->k_count >= 0 &&
+                    d->k_begin + d->k_count <= d->n_s,
+                "bad shard range");
+    IMP_REQUIRE(d->dyn_source, "missing dynamics source");
+    IMP_CUDA(cudaSetDevice(d->device));
+    int sms = 148;
+    IMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
+                                    d->device));
+    JitModule& M = jit(d->device, config_header(d) + d->dyn_source);
+
+    cudaStream_t s;
+    IMP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+    Events ev;
+    IMP_CUDA(cudaEventRecord(ev.e[0], s));
+
+    // --- host geometry -> device ------------------------------------------
+    std::vector<int> edge_off(N), strides(N);
+    int total = 1, off = 0;
+    for (int q = 0; q < N; ++q) {
+      edge_off[q] = off;
+      off += d->counts[q] + 1;
+    }
+    for (int q = N - 1; q >= 0; --q) {
+      strides[q] = total;
+      total *= d->counts[q];
+    }
+    auto flat_of = [&](const int32_t* multi, int cnt) {
+      std::vector<int> f(cnt);
+      for (int i = 0; i < cnt; ++i) {
+        int v = 0;
+        for (int q = 0; q < N; ++q) v += multi[(int64_t)i * N + q] * strides[q];
+        f[i] = v;
+      }
+      return f;
+    };
+    std::vector<int> sflat = flat_of(d->safe_multi, d->n_s);
+    std::vector<int> tflat = flat_of(d->target_multi, d->n_t);
+    std::vector<int> aflat = flat_of(d->avoid_multi, d->n_a);
+    std::vector<int> label;
+    const bool identity = d->n_t == 0 && d->n_a == 0 && d->n_s == total;
+    if (!identity) {
+      label.assign(total, INT32_MIN);
+      for (int i = 0; i < d->n_s; ++i) label[sflat[i]] = i;
+      for (int i = 0; i < d->n_t; ++i) label[tflat[i]] = -1 - i;
+      for (int i = 0; i < d->n_a; ++i) label[aflat[i]] = -1 - d->n_t - i;
+    }
+    auto g_counts = upload(d->counts, N, s);
+    auto g_eoff = upload(edge_off.data(), N, s);
+    auto g_strides = upload(strides.data(), N, s);
+    auto g_eta = upload(d->eta, N, s);
+    auto g_sigma = upload(d->sigma, N, s);
+    auto g_edges = upload(d->edges, (size_t)off, s);
+    auto g_clo = upload(d->cover_lo, N, s);
+    auto g_chi = upload(d->cover_hi, N, s);
+    auto g_slo = upload(d->src_lo, (size_t)d->n_s * N, s);
+    auto g_shi = upload(d->src_hi, (size_t)d->n_s * N, s);
+    const int nc = std::max(d->n_consts, 1);
+    auto g_consts = upload(d->consts, (size_t)d->n_u * d->n_w * nc, s);
+    auto g_label = upload(label.data(), label.size(), s);
+    auto g_sflat = upload(sflat.data(), sflat.size(), s);
+    auto g_tflat = upload(tflat.data(), tflat.size(), s);
+    auto g_aflat = upload(aflat.data(), aflat.size(), s);
+
+    const long long n_rows = (long long)d->k_count * d->n_u * d->n_w;
+    h = new imp_imdp();
+    h->device = d->device;
+    h->n_s = d->n_s;
+    h->n_u = d->n_u;
+    h->n_w = d->n_w;
+    h->k_begin = d->k_begin;
+    h->k_count = d->k_count;
+    h->n_rows = n_rows;
+
+    DevBuf<double> mlo(n_rows * N + 1), mhi(n_rows * N + 1), raw(n_rows * 6 + 1);
+    DevBuf<long long> tcnt(n_rows + 1), xcnt(n_rows + 1);
+    DevBuf<int64_t> row_ptr(n_rows + 1);
+    DevBuf<long long> aux_ptr(n_rows + 1);
+    DevBuf<unsigned long long> err(3);
+    DevBuf<double> err_val(3);
+    DevBuf<long long> evals(1);
+    IMP_CUDA(cudaMemsetAsync(err.ptr, 0xff, 3 * sizeof(unsigned long long), s));
+    IMP_CUDA(cudaMemsetAsync(err_val.ptr, 0, 3 * sizeof(double), s));
+    IMP_CUDA(cudaMemsetAsync(evals.ptr, 0, sizeof(long long), s));
+    IMP_CUDA(cudaMemsetAsync(tcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
+    IMP_CUDA(cudaMemsetAsync(xcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
+    IMP_CUDA(cudaMemsetAsync(raw.ptr, 0, (n_rows * 6 + 1) * sizeof(double), s));
+
+    BuildParams P{};
+    P.n_u = d->n_u;
+    P.n_w = d->n_w;
+    P.k_begin = d->k_begin;
+    P.k_count = d->k_count;
+    P.n_rows = n_rows;
+    P.n_s = d->n_s;
+    P.n_t = d->n_t;
+    P.n_a = d->n_a;
+    P.total = total;
+    P.counts = g_counts.ptr;
+    P.edge_off = g_eoff.ptr;
+    P.strides = g_strides.ptr;
+    P.eta = g_eta.ptr;
+    P.sigma = g_sigma.ptr;
+    P.edges = g_edges.ptr;
+    P.cover_lo = g_clo.ptr;
+    P.cover_hi = g_chi.ptr;
+    P.src_lo = g_slo.ptr;
+    P.src_hi = g_shi.ptr;
+    P.consts = g_consts.ptr;
+    P.label = identity ? nullptr : g_label.ptr;
+    P.safe_flat = g_sflat.ptr;
+    P.target_flat = g_tflat.ptr;
+    P.avoid_flat = g_aflat.ptr;
+    P.cutoff = d->zero_cutoff;
+    P.tol = d->tol;
+    P.low_cost = d->low_cost;
+    P.separable = d->separable;
+    P.max_evals_fixed = d->max_evals_per_dim < 0 ? -d->max_evals_per_dim : 0;
+    P.multistart = d->multistart;
+    P.mlo = mlo.ptr;
+    P.mhi = mhi.ptr;
+    P.t_count = tcnt.ptr;
+    P.x_count = xcnt.ptr;
+    P.row_ptr = reinterpret_cast<const long long*>(row_ptr.ptr);
+    P.aux_ptr = aux_ptr.ptr;
+    P.raw = raw.ptr;
+    P.evals = evals.ptr;
+    P.err = err.ptr;
+    P.err_val = err_val.ptr;
+
+    // --- stage 1: mean ranges -------------------------------------------------
+    const size_t nm_doubles = (size_t)(N + 1) * N + (N + 1);
+    int block1 = 128;
+    while (block1 > 32 && block1 * nm_doubles * 8 > 96 * 1024) block1 -= 32;
+    if (n_rows > 0) {
+      const long long ntask = n_rows * N * 2;
+      unsigned grid = (unsigned)std::min<long long>((ntask + block1 - 1) / block1,
+                                                    (long long)sms * 64);
+      launch(M.mean, grid, block1, block1 * nm_doubles * 8, s, P);
+    }
+    IMP_CUDA(cudaEventRecord(ev.e[1], s));
+
+    // --- stage 2: count, scan, write ---------------------------------------
+    int nbins = 0;
+    for (int q = 0; q < N; ++q) nbins += d->counts[q];
+    const size_t smem2 = 2 * (size_t)nbins * sizeof(double);
+    const unsigned grid2 = (unsigned)std::max<long long>(
+        1, std::min<long long>(n_rows, (long long)sms * 32));
+    P.write = 0;
+    if (n_rows > 0) launch(M.outer, grid2, 128, smem2, s, P);
+    exclusive_scan(tcnt.ptr, reinterpret_cast<long long*>(row_ptr.ptr), n_rows + 1, s);
+    exclusive_scan(xcnt.ptr, aux_ptr.ptr, n_rows + 1, s);
+    long long nnz = 0, naux = 0;
+    IMP_CUDA(cudaMemcpyAsync(&nnz, row_ptr.ptr + n_rows, sizeof(long long),
+                             cudaMemcpyDeviceToHost, s));
+    IMP_CUDA(cudaMemcpyAsync(&naux, aux_ptr.ptr + n_rows, sizeof(long long),
+                             cudaMemcpyDeviceToHost, s));
+    IMP_CUDA(cudaStreamSynchronize(s));
+    h->nnz = nnz;
+    h->col.alloc(std::max<long long>(nnz, 1));
+    h->lo.alloc(std::max<long long>(nnz, 1));
+    h->hi.alloc(std::max<long long>(nnz, 1));
+    DevBuf<int> aux_code(std::max<long long>(naux, 1));
+    DevBuf<double> aux_min(std::max<long long>(naux, 1)),
+        aux_max(std::max<long long>(naux, 1));
+    P.col = h->col.ptr;
+    P.lo = h->lo.ptr;
+    P.hi = h->hi.ptr;
+    P.aux_code = aux_code.ptr;
+    P.aux_min = aux_min.ptr;
+    P.aux_max = aux_max.ptr;
+    P.write = 1;
+    if (n_rows > 0) launch(M.outer, grid2, 128, smem2, s, P);
+    IMP_CUDA(cudaEventRecord(ev.e[2], s));
+
+    // --- stage 3: NM refinement of the live window (coupled) ---------------
+    long long instances = 0;
+    if (!d->separable && n_rows > 0) {
+      P.n_items = nnz + naux + n_rows;
+      instances = 2 * P.n_items;
+      const int block3 = 128;
+      const size_t smem3 = block3 * nm_doubles * sizeof(double);
+      const void* rfn = reinterpret_cast<const void*>(M.refine);
+      if (smem3 > 48 * 1024)
+        IMP_CUDA(cudaFuncSetAttribute(
+            rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+      int per_sm = 0;
+      IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rfn,
+                                                             block3, smem3));
+      per_sm = std::max(per_sm, 1);
+      const long long need = (instances + block3 - 1) / block3;
+      const unsigned grid3 = (unsigned)std::max<long long>(
+          1, std::min<long long>(need, (long long)sms * per_sm));
+      launch(M.refine, grid3, block3, smem3, s, P);
+    }
+    IMP_CUDA(cudaEventRecord(ev.e[3], s));
+
+    // --- stage 4: assemble ---------------------------------------------------
+    for (auto* b : {&h->r_min, &h->r_max, &h->a_min, &h->a_max})
+      b->alloc(std::max<long long>(n_rows, 1));
+    P.r_min = h->r_min.ptr;
+    P.r_max = h->r_max.ptr;
+    P.a_min = h->a_min.ptr;
+    P.a_max = h->a_max.ptr;
+    if (n_rows > 0) {
+      const unsigned grid4 = (unsigned)std::max<long long>(
+          1, std::min<long long>((n_rows * 32 + 255) / 256, (long long)sms * 64));
+      launch(M.assemble, grid4, 256, 0, s, P);
+    }
+    IMP_CUDA(cudaEventRecord(ev.e[4], s));
+    IMP_CUDA(cudaStreamSynchronize(s));
+
+    unsigned long long herr[3];
+    double hval[3];
+    long long hev = 0;
+    IMP_CUDA(cudaMemcpy(herr, err.ptr, sizeof(herr), cudaMemcpyDeviceToHost));
+    IMP_CUDA(cudaMemcpy(hval, err_val.ptr, sizeof(hval), cudaMemcpyDeviceToHost));
+    IMP_CUDA(cudaMemcpy(&hev, evals.ptr, sizeof(hev), cudaMemcpyDeviceToHost));
+    const long long row0 = (long long)d->k_begin * d->n_u * d->n_w;
+    if (herr[0] != ~0ull) {
+      set_error("row %lld", row0 + (long long)herr[0]);
+      throw Failure{IMP_E_NONFINITE};
+    }
+    if (herr[1] != ~0ull) {
+      set_error("row %lld: min-side sum exceeds 1 by %.17g",
+                row0 + (long long)herr[1], hval[1]);
+      throw Failure{IMP_E_ABSTRACTION};
+    }
+    if (herr[2] != ~0ull) {
+      set_error("row %lld: max-side sum falls short of 1 by %.17g",
+                row0 + (long long)herr[2], hval[2]);
+      throw Failure{IMP_E_ABSTRACTION};
+    }
+    h->row_ptr = std::move(row_ptr);
+    finalize_imdp(h, s);
+    IMP_CUDA(cudaEventRecord(ev.e[5], s));
+    IMP_CUDA(cudaEventSynchronize(ev.e[5]));
+    if (stats) {
+      stats->ms_total = ev.ms(0, 5);
+      stats->ms_mean_ranges = ev.ms(0, 1);
+      stats->ms_outer = ev.ms(1, 2);
+      stats->ms_refine = ev.ms(2, 3);
+      stats->ms_assemble = ev.ms(3, 5);
+      stats->nnz = nnz;
+      stats->nm_instances = instances;
+      stats->nm_evals = hev;
+    }
+    *out = h;
+  });
+  if (st != IMP_OK) delete h;
+  return st;
+}
+
+// Compile (only) the construction module for a dynamics spec and optionally
+// write the cubin to `cubin_path`: used by the CPU build check and to
+// inspect SASS (cuobjdump) without a GPU.
+extern "C" int imp_jit_compile(const imp_build_desc* d, const char* cubin_path) {
+  return guarded([&] {
+    IMP_REQUIRE(d && d->dyn_source, "null argument");
+    std::vector<char> cubin = compile_cubin(jit_source(config_header(d) + d->dyn_source));
+    if (cubin_path) {
+      FILE* f = fopen(cubin_path, "wb");
+      IMP_REQUIRE(f, "cannot open %s", cubin_path);
+      fwrite(cubin.data(), 1, cubin.size(), f);
+      fclose(f);
+    }
+  });
 }

@@ -1,2 +1,864 @@
-// placeholder; replaced by the construction kernels
-#pragma once
+// IMDP construction kernels, JIT-compiled by NVRTC per dynamics spec.
+//
+// The module source is  ndtr.h + <generated config> + <generated dynamics>
+// + this file.  The generated config defines
+//   IMP_N, IMP_NC             state dimension, folded constants per (j, i)
+//   kNDeps[IMP_N]             state dependencies of each f_d
+//   kDeps[IMP_N][IMP_N]       their indices (ascending, -1 padded)
+// and the dynamics provide imp_f<d>(x, k) / imp_fd(d, x, k), x = full state
+// vector, k = the row's folded x-free subexpressions.  Compiled with
+// --fmad=false so every expression, centroid and Horner step rounds like
+// the reference's numpy evaluation.
+//
+// Stages (reference pkg/src/impact/abstraction.py):
+//   1 k_mean_ranges  per (row, d, sign): NM over the dependency sub-cell,
+//                    min over starts                       (:256-284)
+//   2 k_outer        per row (CTA): exact per-dimension extremes (:287-297),
+//                    pruned enumeration of the lattice box whose outer
+//                    product can exceed the cutoff, cutoff / live window,
+//                    CSR count + write (two launches), separable values,
+//                    r / a terms and cover leak           (:442-508, :300-319)
+//   3 k_refine       coupled dynamics: one thread per NM instance
+//                    (row, live box, min|max) running all `multistart`
+//                    starts through a one-evaluation-per-step state machine,
+//                    simplex held in shared memory      (:322-375, :465-495;
+//                                                        optimize.py:47-155)
+//   4 k_assemble     clip, low-cost, row-sum repair, hard errors (:607-659)
+
+#define IMP_INF __longlong_as_double(0x7ff0000000000000ll)
+
+__device__ __forceinline__ double imp_min(double a, double b) {
+  return (a < b || a != a) ? a : b;   // numpy.minimum propagates NaN
+}
+__device__ __forceinline__ double imp_max(double a, double b) {
+  return (a > b || a != a) ? a : b;
+}
+__device__ __forceinline__ double imp_clip(double x, double lo, double hi) {
+  return fmin(fmax(x, lo), hi);       // np.clip on finite values
+}
+__device__ __forceinline__ bool imp_finite(double x) {
+  return x - x == 0.0;
+}
+
+struct BuildParams {
+  int n_u, n_w, k_begin, k_count;
+  long long n_rows;
+  int n_s, n_t, n_a, total;
+  const int* counts;          // (N)
+  const int* edge_off;        // (N) offsets into edges
+  const int* strides;         // (N) flat-index strides (row-major)
+  const double* eta;          // (N)
+  const double* sigma;        // (N)
+  const double* edges;
+  const double* cover_lo;
+  const double* cover_hi;
+  const double* src_lo;       // (n_s, N) clipped source cells, global k
+  const double* src_hi;
+  const double* consts;       // (n_u * n_w, NC)
+  const int* label;           // (total) >= 0 safe pos, -1-t target,
+                              // -1-n_t-a avoid; nullptr: every point safe
+  const int* safe_flat;       // (n_s)
+  const int* target_flat;     // (n_t)
+  const int* avoid_flat;      // (n_a)
+  double cutoff, tol;
+  int low_cost, separable;
+  int max_evals_fixed;        // 0: 200 * dim
+  int multistart;             // 0: 1 + 2 * dim
+  // stage 1
+  double* mlo;                // (n_rows, N)
+  double* mhi;
+  // stage 2
+  int write;                  // 0: count pass, 1: write pass
+  long long* t_count;         // (n_rows) count pass output
+  long long* x_count;         // (n_rows) aux items (coupled)
+  const long long* row_ptr;   // (n_rows + 1)
+  const long long* aux_ptr;   // (n_rows + 1)
+  int* col;
+  double* lo;
+  double* hi;
+  int* aux_code;              // >= 0 target index, < 0: -1 - avoid index
+  double* aux_min;
+  double* aux_max;
+  double* raw;                // (n_rows, 6): r_min r_max av_min av_max
+                              //              leak_min leak_max
+  // stage 3
+  long long n_items;          // nnz + n_aux + n_rows
+  long long* evals;           // total objective evaluations (atomic)
+  // stage 4
+  double* r_min;
+  double* r_max;
+  double* a_min;
+  double* a_max;
+  // errors
+  unsigned long long* err;    // [0]: first non-finite row, [1]: first
+                              // min-side excess row, [2]: max-side deficit
+  double* err_val;            // [1], [2]: the offending magnitudes
+};
+
+__device__ __forceinline__ int imp_max_evals(const BuildParams& P, int dim) {
+  return P.max_evals_fixed ? P.max_evals_fixed : 200 * (dim > 1 ? dim : 1);
+}
+__device__ __forceinline__ int imp_multistart(const BuildParams& P, int dim) {
+  return P.multistart ? P.multistart : 1 + 2 * dim;
+}
+
+__device__ __forceinline__ void imp_row_kji(const BuildParams& P, long long r,
+                                            int& k, int& j, int& i) {
+  i = (int)(r % P.n_w);
+  long long rest = r / P.n_w;
+  j = (int)(rest % P.n_u);
+  k = P.k_begin + (int)(rest / P.n_u);
+}
+
+// Deterministic start list (optimize.py:28-44) for a D-dim box.
+template <int D>
+__device__ __forceinline__ void imp_start_point(const double* lo,
+                                                const double* hi, int s,
+                                                double* out) {
+  double c[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) c[d] = (lo[d] + hi[d]) / 2;
+  int b = s;
+  if (s > 2 * D) b = (s - 2 * D) % (1 + 2 * D);
+#pragma unroll
+  for (int d = 0; d < D; ++d) out[d] = c[d];
+  if (b > 0) {
+    int dd = (b - 1) >> 1;
+    bool up = (b - 1) & 1;
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (d == dd) out[d] = up ? hi[d] : lo[d];
+  }
+  if (s > 2 * D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) out[d] = (out[d] + c[d]) / 2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Nelder-Mead (optimize.py:47-155) as a one-evaluation-per-step state
+// machine.  point() gives the next point to evaluate, feed() consumes its
+// objective value.  The simplex lives in shared memory (dynamic vertex
+// indexing, conflict-free stride = block size); centroid / candidates stay
+// in registers.
+// ---------------------------------------------------------------------------
+enum { NM_INIT = 0, NM_REFLECT = 1, NM_SECOND = 2, NM_SHRINK = 3 };
+enum { NM_EXPAND = 0, NM_OUTSIDE = 1, NM_INSIDE = 2 };
+
+template <int D>
+struct NelderMead {
+  double* X;   // X[(v * D + d) * S]
+  double* F;   // F[v * S]
+  int S;
+  double lo[D], hi[D];
+  double c[D], xr[D], cand[D];
+  double fr, tol, best;
+  int phase, v, evals, kind, max_evals;
+  bool done;
+
+  __device__ __forceinline__ double& x(int vv, int d) { return X[(vv * D + d) * S]; }
+  __device__ __forceinline__ double& f(int vv) { return F[vv * S]; }
+
+  __device__ void start(const double* s) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) x(0, d) = s[d];
+#pragma unroll
+    for (int e = 0; e < D; ++e) {
+      const double step = 0.25 * (hi[e] - lo[e]);
+#pragma unroll
+      for (int d = 0; d < D; ++d) x(e + 1, d) = s[d];
+      const double up = s[e] + step;
+      x(e + 1, e) = up <= hi[e] ? up : s[e] - step;
+    }
+    phase = NM_INIT;
+    v = 0;
+    evals = 0;
+    done = false;
+  }
+
+  __device__ __forceinline__ void point(double* p) {
+    if (phase == NM_REFLECT) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) p[d] = xr[d];
+    } else if (phase == NM_SECOND) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) p[d] = cand[d];
+    } else {
+#pragma unroll
+      for (int d = 0; d < D; ++d) p[d] = x(v, d);
+    }
+  }
+
+  __device__ void accept(const double* p, double fp) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) x(D, d) = p[d];
+    f(D) = fp;
+  }
+
+  __device__ void iterate() {
+    // stable insertion sort of the vertices by value
+    for (int i = 1; i <= D; ++i) {
+      for (int j = i; j > 0 && f(j) < f(j - 1); --j) {
+        double t = f(j);
+        f(j) = f(j - 1);
+        f(j - 1) = t;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          double u = x(j, d);
+          x(j, d) = x(j - 1, d);
+          x(j - 1, d) = u;
+        }
+      }
+    }
+    const double spread = f(D) - f(0);
+    if (!(spread > tol && evals < max_evals)) {
+      done = true;
+      best = f(0);
+      return;
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      double s = x(0, d);
+      for (int vv = 1; vv < D; ++vv) s += x(vv, d);
+      c[d] = s / D;
+      xr[d] = imp_clip(c[d] + 1.0 * (c[d] - x(D, d)), lo[d], hi[d]);
+    }
+    phase = NM_REFLECT;
+  }
+
+  __device__ void feed(double fp) {
+    switch (phase) {
+      case NM_INIT:
+        f(v) = fp;
+        if (++v <= D) return;
+        evals = D + 1;
+        iterate();
+        return;
+      case NM_REFLECT: {
+        fr = fp;
+        evals += 1;
+        if (fr < f(0)) {
+          kind = NM_EXPAND;
+#pragma unroll
+          for (int d = 0; d < D; ++d)
+            cand[d] = imp_clip(c[d] + 2.0 * (c[d] - x(D, d)), lo[d], hi[d]);
+          phase = NM_SECOND;
+          return;
+        }
+        if (fr >= f(D - 1)) {
+          if (fr < f(D)) {
+            kind = NM_OUTSIDE;
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+              cand[d] = imp_clip(c[d] + 0.5 * (xr[d] - c[d]), lo[d], hi[d]);
+          } else {
+            kind = NM_INSIDE;
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+              cand[d] = imp_clip(c[d] + 0.5 * (x(D, d) - c[d]), lo[d], hi[d]);
+          }
+          phase = NM_SECOND;
+          return;
+        }
+        accept(xr, fr);
+        iterate();
+        return;
+      }
+      case NM_SECOND: {
+        evals += 1;
+        if (kind == NM_EXPAND) {
+          if (fp < fr) accept(cand, fp);
+          else accept(xr, fr);
+          iterate();
+          return;
+        }
+        if (kind == NM_OUTSIDE ? (fp < fr) : (fp < f(D))) {
+          accept(cand, fp);
+          iterate();
+          return;
+        }
+        for (int vv = 1; vv <= D; ++vv) {
+#pragma unroll
+          for (int d = 0; d < D; ++d)
+            x(vv, d) = x(0, d) + 0.5 * (x(vv, d) - x(0, d));
+        }
+        v = 1;
+        phase = NM_SHRINK;
+        return;
+      }
+      default:  // NM_SHRINK
+        f(v) = fp;
+        if (++v <= D) return;
+        evals += D;
+        iterate();
+        return;
+    }
+  }
+};
+
+__device__ __forceinline__ void imp_flag_nonfinite(const BuildParams& P,
+                                                   long long row) {
+  atomicMin(P.err, (unsigned long long)row);
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1: per-dimension mean ranges (abstraction.py:256-284)
+// ---------------------------------------------------------------------------
+
+template <int DI>
+__device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
+                                   double* smem, int S) {
+  constexpr int D = kNDeps[DI];
+  int k, j, i;
+  imp_row_kji(P, r, k, j, i);
+  const double* K = P.consts + (long long)(j * P.n_w + i) * IMP_NC;
+  double xfull[IMP_N];
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) xfull[d] = 0.0;
+  if constexpr (D == 0) {
+    double v = imp_fd(DI, xfull, K);
+    if (!imp_finite(v)) imp_flag_nonfinite(P, r);
+    if (sgn == 0) P.mlo[r * IMP_N + DI] = v;
+    else P.mhi[r * IMP_N + DI] = v;
+    return 0;
+  } else {
+    NelderMead<D> nm;
+    nm.X = smem;
+    nm.F = smem + (D + 1) * D * S;
+    nm.S = S;
+    nm.tol = P.tol;
+    nm.max_evals = imp_max_evals(P, D);
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      nm.lo[q] = P.src_lo[(long long)k * IMP_N + kDeps[DI][q]];
+      nm.hi[q] = P.src_hi[(long long)k * IMP_N + kDeps[DI][q]];
+    }
+    const int ms = imp_multistart(P, D);
+    const double sign = sgn ? -1.0 : 1.0;
+    double best = IMP_INF;
+    long long ev = 0;
+    for (int s = 0; s < ms; ++s) {
+      double st[D];
+      imp_start_point<D>(nm.lo, nm.hi, s, st);
+      nm.start(st);
+      while (!nm.done) {
+        double p[D];
+        nm.point(p);
+#pragma unroll
+        for (int q = 0; q < D; ++q) xfull[kDeps[DI][q]] = p[q];
+        double val = imp_fd(DI, xfull, K) * sign;
+        if (!imp_finite(val)) {
+          imp_flag_nonfinite(P, r);
+          val = 0.0;
+        }
+        nm.feed(val);
+        ++ev;
+      }
+      best = fmin(best, nm.best);
+    }
+    if (sgn == 0) P.mlo[r * IMP_N + DI] = best;
+    else P.mhi[r * IMP_N + DI] = -best;
+    return ev;
+  }
+}
+
+template <int DI>
+__device__ __forceinline__ long long imp_mean_dispatch(int d,
+                                                       const BuildParams& P,
+                                                       long long r, int sgn,
+                                                       double* smem, int S) {
+  if constexpr (DI < IMP_N) {
+    if (d == DI) return imp_mean_task<DI>(P, r, sgn, smem, S);
+    return imp_mean_dispatch<DI + 1>(d, P, r, sgn, smem, S);
+  }
+  return 0;
+}
+
+extern "C" __global__ void k_mean_ranges(BuildParams P) {
+  extern __shared__ double smem[];
+  const int S = blockDim.x;
+  const long long ntask = P.n_rows * IMP_N * 2;
+  unsigned long long ev = 0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       t < ntask; t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t % P.n_rows;
+    const int ds = (int)(t / P.n_rows);
+    ev += imp_mean_dispatch<0>(ds >> 1, P, r, ds & 1, smem + threadIdx.x, S);
+  }
+  if (ev) atomicAdd((unsigned long long*)P.evals, ev);
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2: per-row extremes tables, pruned lattice enumeration, CSR
+// ---------------------------------------------------------------------------
+
+// Deterministic block sum (fixed tree over the block, result in all threads).
+__device__ double imp_block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  v = lane < nw ? red[lane] : 0.0;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+// Block exclusive scan of 0/1 flags; returns this thread's offset, *total
+// gets the block count.
+__device__ int imp_block_scan(int flag, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(0xffffffffu, flag);
+  const int pre = __popc(b & ((1u << lane) - 1u));
+  __syncthreads();
+  if (lane == 0) wsum[w] = __popc(b);
+  __syncthreads();
+  int off = 0, tot = 0;
+  const int nw = blockDim.x >> 5;
+  for (int q = 0; q < nw; ++q) {
+    int c = wsum[q];
+    if (q < w) off += c;
+    tot += c;
+  }
+  *total = tot;
+  return off + pre;
+}
+
+struct RowTables {
+  double* gmin;   // per dim d: [edge_off[d] - d, + counts[d])
+  double* gmax;
+  int blo[IMP_N], bext[IMP_N];
+  long long box;
+};
+
+extern "C" __global__ void k_outer(BuildParams P) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ int wsum[32];
+  __shared__ int s_blo[IMP_N], s_bext[IMP_N];
+  __shared__ double s_ml[IMP_N], s_mh[IMP_N];
+  int nbins = 0;
+  for (int d = 0; d < IMP_N; ++d) nbins += P.counts[d];
+  double* gmin = smem;
+  double* gmax = smem + nbins;
+
+  for (long long r = blockIdx.x; r < P.n_rows; r += gridDim.x) {
+    if (threadIdx.x < IMP_N) {
+      s_ml[threadIdx.x] = P.mlo[r * IMP_N + threadIdx.x];
+      s_mh[threadIdx.x] = P.mhi[r * IMP_N + threadIdx.x];
+    }
+    __syncthreads();
+    // exact per-dimension extremes (abstraction.py:287-297)
+    {
+      int d = 0, base = 0;
+      for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+        while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
+        const int q = b - base;
+        const double* e = P.edges + P.edge_off[d];
+        const double s = P.sigma[d], ml = s_ml[d], mh = s_mh[d];
+        const double plo = imp_interval_prob(s, ml, e[q], e[q + 1]);
+        const double phi = imp_interval_prob(s, mh, e[q], e[q + 1]);
+        const double mid = (e[q] + e[q + 1]) / 2;
+        double top;
+        if (mid < ml) top = plo;
+        else if (mid > mh) top = phi;
+        else top = imp_interval_prob(s, 0.0, -P.eta[d] / 2, P.eta[d] / 2);
+        gmin[b] = fmin(plo, phi);
+        gmax[b] = top;
+        d = 0;
+        base = 0;
+      }
+    }
+    __syncthreads();
+    // pruned box: a lattice point can only pass the cutoff if every factor
+    // exceeds cutoff / prod_{e != d} max gmax_e (factors are <= 1); the
+    // superlevel sets of the unimodal gmax_d are index intervals.
+    if (threadIdx.x == 0) {
+      double pm[IMP_N];
+      int base = 0;
+      for (int d = 0; d < IMP_N; ++d) {
+        double m = 0.0;
+        for (int q = 0; q < P.counts[d]; ++q) m = fmax(m, gmax[base + q]);
+        pm[d] = m;
+        base += P.counts[d];
+      }
+      base = 0;
+      for (int d = 0; d < IMP_N; ++d) {
+        double rest = 1.0;
+        for (int e = 0; e < IMP_N; ++e)
+          if (e != d) rest *= pm[e];
+        const double thr = P.cutoff * (1.0 - 1e-9) / rest;
+        int lo = P.counts[d], hi = -1;
+        for (int q = 0; q < P.counts[d]; ++q)
+          if (gmax[base + q] > thr) { lo = min(lo, q); hi = q; }
+        s_blo[d] = lo;
+        s_bext[d] = hi >= lo ? hi - lo + 1 : 0;
+        base += P.counts[d];
+      }
+    }
+    __syncthreads();
+    long long box = 1;
+    for (int d = 0; d < IMP_N; ++d) box *= s_bext[d];
+
+    // --- safe destinations: t entries ------------------------------------
+    long long out = P.write ? P.row_ptr[r] : 0;
+    long long cnt = 0;
+    for (long long q0 = 0; q0 < box; q0 += blockDim.x) {
+      const long long q = q0 + threadIdx.x;
+      int live = 0, pos = -1;
+      double tmin = 0.0, tmax = 0.0;
+      if (q < box) {
+        long long rem = q;
+        int flat = 0;
+        int bidx[IMP_N];
+#pragma unroll
+        for (int d = IMP_N - 1; d >= 0; --d) {
+          const int b = s_blo[d] + (int)(rem % s_bext[d]);
+          rem /= s_bext[d];
+          bidx[d] = b;
+          flat += b * P.strides[d];
+        }
+        pos = P.label ? P.label[flat] : flat;
+        if (pos >= 0) {
+          int base = 0;
+#pragma unroll
+          for (int d = 0; d < IMP_N; ++d) {
+            const double a = gmax[base + bidx[d]], c = gmin[base + bidx[d]];
+            tmax = d == 0 ? a : tmax * a;
+            tmin = d == 0 ? c : tmin * c;
+            base += P.counts[d];
+          }
+          live = tmax > P.cutoff;
+        }
+      }
+      int tot;
+      const int off = imp_block_scan(live, wsum, &tot);
+      if (P.write && live) {
+        const long long at = out + cnt + off;
+        P.col[at] = pos;
+        if (P.separable) {
+          P.lo[at] = fmin(tmin, tmax);
+          P.hi[at] = tmax;
+        }
+      }
+      cnt += tot;
+    }
+    if (!P.write && threadIdx.x == 0) P.t_count[r] = cnt;
+
+    // --- target / avoid masses: full lists ------------------------------
+    double rs[2] = {0.0, 0.0}, as[2] = {0.0, 0.0};
+    long long xo = P.write && !P.separable ? P.aux_ptr[r] : 0;
+    long long xc = 0;
+    for (int kind = 0; kind < 2; ++kind) {
+      const int n_list = kind == 0 ? P.n_t : P.n_a;
+      const int* flats = kind == 0 ? P.target_flat : P.avoid_flat;
+      for (int q0 = 0; q0 < n_list; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        double tmin = 0.0, tmax = 0.0;
+        int live = 0;
+        if (q < n_list) {
+          int flat = flats[q];
+          int base = 0;
+#pragma unroll
+          for (int d = 0; d < IMP_N; ++d) {
+            const int b = (flat / P.strides[d]) % P.counts[d];
+            const double a = gmax[base + b], c = gmin[base + b];
+            tmax = d == 0 ? a : tmax * a;
+            tmin = d == 0 ? c : tmin * c;
+            base += P.counts[d];
+          }
+          live = tmax > P.cutoff;
+          if (kind == 0) { rs[0] += tmin; rs[1] += tmax; }
+          else { as[0] += tmin; as[1] += tmax; }
+        }
+        if (!P.separable) {
+          int tot;
+          const int off = imp_block_scan(live, wsum, &tot);
+          if (P.write && live)
+            P.aux_code[xo + xc + off] = kind == 0 ? q : -1 - q;
+          xc += tot;
+        }
+      }
+    }
+    if (!P.write && !P.separable && threadIdx.x == 0) P.x_count[r] = xc;
+
+    if (P.write && P.separable) {
+      const double r0 = imp_block_sum(rs[0], red);
+      const double r1 = imp_block_sum(rs[1], red);
+      const double a0 = imp_block_sum(as[0], red);
+      const double a1 = imp_block_sum(as[1], red);
+      if (threadIdx.x == 0) {
+        // cover leak (abstraction.py:300-309)
+        double pmax = 1.0, pmin = 1.0;
+        for (int d = 0; d < IMP_N; ++d) {
+          const double lo = P.cover_lo[d], hi = P.cover_hi[d];
+          const double mu = imp_clip((lo + hi) / 2, s_ml[d], s_mh[d]);
+          const double s = P.sigma[d];
+          const double pa = imp_interval_prob(s, mu, lo, hi);
+          const double pl = imp_interval_prob(s, s_ml[d], lo, hi);
+          const double ph = imp_interval_prob(s, s_mh[d], lo, hi);
+          pmax = d == 0 ? pa : pmax * pa;
+          pmin = d == 0 ? fmin(pl, ph) : pmin * fmin(pl, ph);
+        }
+        double* raw = P.raw + r * 6;
+        raw[0] = r0;
+        raw[1] = r1;
+        raw[2] = a0;
+        raw[3] = a1;
+        raw[4] = fmax(0.0, 1.0 - pmax);
+        raw[5] = fmax(0.0, 1.0 - pmin);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 3: coupled refinement, one thread per NM instance
+// ---------------------------------------------------------------------------
+
+struct Instance {
+  long long row;
+  int sgn;
+  int kind;          // 0: t entry, 1: aux (target/avoid), 2: cover
+  long long slot;    // CSR / aux index
+  double blo[IMP_N], bhi[IMP_N];
+  double clo[IMP_N], chi[IMP_N];
+  const double* K;
+};
+
+__device__ void imp_setup_instance(const BuildParams& P, long long g,
+                                   Instance& I) {
+  const long long item = g >> 1;
+  I.sgn = (int)(g & 1);
+  // row = largest r with item_ptr[r] <= item, item_ptr = row_ptr + aux_ptr + r
+  long long lo = 0, hi = P.n_rows - 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) >> 1;
+    if (P.row_ptr[mid] + P.aux_ptr[mid] + mid <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  const long long r = lo;
+  I.row = r;
+  const long long rel = item - (P.row_ptr[r] + P.aux_ptr[r] + r);
+  const long long nt = P.row_ptr[r + 1] - P.row_ptr[r];
+  const long long nx = P.aux_ptr[r + 1] - P.aux_ptr[r];
+  int flat = -1;
+  if (rel < nt) {
+    I.kind = 0;
+    I.slot = P.row_ptr[r] + rel;
+    flat = P.safe_flat[P.col[I.slot]];
+  } else if (rel < nt + nx) {
+    I.kind = 1;
+    I.slot = P.aux_ptr[r] + (rel - nt);
+    const int code = P.aux_code[I.slot];
+    flat = code >= 0 ? P.target_flat[code] : P.avoid_flat[-1 - code];
+  } else {
+    I.kind = 2;
+    I.slot = r;
+  }
+  if (flat >= 0) {
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d) {
+      const int b = (flat / P.strides[d]) % P.counts[d];
+      const double* e = P.edges + P.edge_off[d];
+      I.blo[d] = e[b];
+      I.bhi[d] = e[b + 1];
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d) {
+      I.blo[d] = P.cover_lo[d];
+      I.bhi[d] = P.cover_hi[d];
+    }
+  }
+  int k, j, i;
+  imp_row_kji(P, r, k, j, i);
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) {
+    I.clo[d] = P.src_lo[(long long)k * IMP_N + d];
+    I.chi[d] = P.src_hi[(long long)k * IMP_N + d];
+  }
+  I.K = P.consts + (long long)(j * P.n_w + i) * IMP_NC;
+}
+
+// P(f(x) + noise in box) * sign  (abstraction.py:333-349)
+__device__ __forceinline__ double imp_box_objective(const BuildParams& P,
+                                                    const Instance& I,
+                                                    const double* x) {
+  double prob = 1.0;
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) {
+    const double m = imp_fd(d, x, I.K);
+    prob *= imp_interval_prob(P.sigma[d], m, I.blo[d], I.bhi[d]);
+  }
+  return I.sgn ? prob * -1.0 : prob;
+}
+
+__device__ void imp_store_instance(const BuildParams& P, const Instance& I,
+                                   double best) {
+  const double v = I.sgn ? -best : best;
+  if (I.kind == 0) {
+    if (I.sgn) P.hi[I.slot] = v;
+    else P.lo[I.slot] = v;
+  } else if (I.kind == 1) {
+    if (I.sgn) P.aux_max[I.slot] = v;
+    else P.aux_min[I.slot] = v;
+  } else {
+    // cover: leak bounds from the box probability extremes
+    double* raw = P.raw + I.row * 6;
+    if (I.sgn) raw[4] = fmax(0.0, 1.0 - v);   // leak_min = 1 - p_max
+    else raw[5] = fmax(0.0, 1.0 - v);         // leak_max = 1 - p_min
+  }
+}
+
+extern "C" __global__ void __launch_bounds__(128) k_refine(BuildParams P) {
+  extern __shared__ double smem[];
+  const int S = blockDim.x;
+  NelderMead<IMP_N> nm;
+  nm.X = smem + threadIdx.x;
+  nm.F = smem + (IMP_N + 1) * IMP_N * S + threadIdx.x;
+  nm.S = S;
+  nm.tol = P.tol;
+  nm.max_evals = imp_max_evals(P, IMP_N);
+  const int ms = imp_multistart(P, IMP_N);
+  const long long total = 2 * P.n_items;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= total) return;
+  Instance I;
+  imp_setup_instance(P, g, I);
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) {
+    nm.lo[d] = I.clo[d];
+    nm.hi[d] = I.chi[d];
+  }
+  int s = 0;
+  double best = IMP_INF;
+  unsigned long long ev = 0;
+  {
+    double st[IMP_N];
+    imp_start_point<IMP_N>(nm.lo, nm.hi, 0, st);
+    nm.start(st);
+  }
+  for (;;) {
+    double p[IMP_N];
+    nm.point(p);
+    double val = imp_box_objective(P, I, p);
+    if (!imp_finite(val)) {
+      imp_flag_nonfinite(P, I.row);
+      val = 0.0;
+    }
+    ++ev;
+    nm.feed(val);
+    if (!nm.done) continue;
+    best = fmin(best, nm.best);
+    if (++s == ms) {
+      imp_store_instance(P, I, best);
+      g += stride;
+      if (g >= total) break;
+      imp_setup_instance(P, g, I);
+#pragma unroll
+      for (int d = 0; d < IMP_N; ++d) {
+        nm.lo[d] = I.clo[d];
+        nm.hi[d] = I.chi[d];
+      }
+      s = 0;
+      best = IMP_INF;
+    }
+    double st[IMP_N];
+    imp_start_point<IMP_N>(nm.lo, nm.hi, s, st);
+    nm.start(st);
+  }
+  atomicAdd((unsigned long long*)P.evals, ev);
+}
+
+// ---------------------------------------------------------------------------
+// Stage 4: assemble (abstraction.py:607-659), one warp per row
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double imp_warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
+extern "C" __global__ void k_assemble(BuildParams P) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = w0; r < P.n_rows; r += nw) {
+    const long long b = P.row_ptr[r], e = P.row_ptr[r + 1];
+    double* raw = P.raw + r * 6;
+    double rmin, rmax, avmin, avmax;
+    if (P.separable) {
+      rmin = raw[0]; rmax = raw[1]; avmin = raw[2]; avmax = raw[3];
+    } else {
+      // sums of the refined target / avoid terms (non-live terms are 0)
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      const long long xb = P.aux_ptr[r], xe = P.aux_ptr[r + 1];
+      for (long long q = xb + lane; q < xe; q += 32) {
+        const int code = P.aux_code[q];
+        const int off = code >= 0 ? 0 : 2;
+        s[off] += P.aux_min[q];
+        s[off + 1] += P.aux_max[q];
+      }
+      rmin = imp_warp_sum(s[0]);
+      rmax = imp_warp_sum(s[1]);
+      avmin = imp_warp_sum(s[2]);
+      avmax = imp_warp_sum(s[3]);
+    }
+    // clip t entries, t_min = min(t_min, t_max), low-cost zeroing
+    double smin = 0.0, smax = 0.0;
+    for (long long q = b + lane; q < e; q += 32) {
+      double hi = imp_clip(P.hi[q], 0.0, 1.0);
+      double lo = imp_clip(P.lo[q], 0.0, 1.0);
+      if (P.low_cost && hi <= P.cutoff) lo = 0.0;
+      lo = fmin(lo, hi);
+      P.lo[q] = lo;
+      P.hi[q] = hi;
+      smin += lo;
+      smax += hi;
+    }
+    smin = imp_warp_sum(smin);
+    smax = imp_warp_sum(smax);
+    rmin = imp_clip(rmin, 0.0, 1.0);
+    rmax = imp_clip(rmax, 0.0, 1.0);
+    rmin = fmin(rmin, rmax);
+    avmin = imp_clip(avmin, 0.0, 1.0);
+    avmax = imp_clip(avmax, 0.0, 1.0);
+    avmin = fmin(avmin, avmax);
+    double lkmin = imp_clip(raw[4], 0.0, 1.0), lkmax = imp_clip(raw[5], 0.0, 1.0);
+    lkmin = fmin(lkmin, lkmax);
+    double amin = imp_clip(lkmin + avmin, 0.0, 1.0);
+    double amax = imp_clip(lkmax + avmax, 0.0, 1.0);
+    // row-sum repair: shave min-side excess off a_min, then scale
+    const double excess = fmax(smin + rmin + amin - 1.0, 0.0);
+    if (excess > 1e-6 && lane == 0) {
+      if (atomicMin(P.err + 1, (unsigned long long)r) > (unsigned long long)r)
+        P.err_val[1] = excess;
+    }
+    const double shaved = fmin(excess, amin);
+    amin = amin - shaved;
+    const double rest = excess - shaved;
+    if (rest > 0) {
+      const double s = smin + rmin;
+      const double scale = s > 0 ? 1.0 - rest / fmax(s, 1e-300) : 1.0;
+      for (long long q = b + lane; q < e; q += 32) P.lo[q] *= scale;
+      rmin *= scale;
+    }
+    const double deficit = fmax(1.0 - (smax + rmax + amax), 0.0);
+    if (deficit > 1e-6 && lane == 0) {
+      if (atomicMin(P.err + 2, (unsigned long long)r) > (unsigned long long)r)
+        P.err_val[2] = deficit;
+    }
+    amax = fmin(amax + deficit, 1.0);
+    amin = fmin(amin, amax);
+    if (lane == 0) {
+      P.r_min[r] = rmin;
+      P.r_max[r] = rmax;
+      P.a_min[r] = amin;
+      P.a_max[r] = amax;
+    }
+  }
+}

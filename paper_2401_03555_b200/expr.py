@@ -424,3 +424,25 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
     deps = [sorted(dyn.state_dependencies(d)) for d in range(n)]
     return LoweredDynamics(source=src, n_consts=len(folded), consts=consts,
                            deps=deps)
+
+
+def has_x_transcendental(dyn: DynamicsSpec) -> bool:
+    """True when some f_d applies a library function (sin, exp, ...) or a
+    power to an x-dependent argument.  Those calls are CUDA's on the device
+    and numpy's (SIMD) in the reference, so construction parity for such
+    dynamics is tolerance-level instead of bitwise (parity)."""
+    def walk(node):
+        tag = node[0]
+        if tag == "call":
+            if any(v.startswith("x") for v in _vars(node, set())):
+                return True
+            return any(walk(a) for a in node[2])
+        if tag == "bin":
+            if node[1] == "^" and any(v.startswith("x")
+                                      for v in _vars(node, set())):
+                return True
+            return walk(node[2]) or walk(node[3])
+        if tag == "neg":
+            return walk(node[1])
+        return False
+    return any(walk(e.node) for e in dyn.exprs)
