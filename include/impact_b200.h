@@ -227,6 +227,16 @@ int imp_shard_sweep(imp_imdp* h, const double* v0, const double* v1,
  * (GFLOP/s, 2 flops per DFMA) measured with CUDA events. */
 int imp_fp64_peak(int device, double* gflops);
 
+/* K5 sweep kernel alone: mean device milliseconds of one twin sweep over
+ * all of h's rows (reps back-to-back launches, CUDA events) -- the HBM
+ * roofline measurement. */
+int imp_time_sweep(imp_imdp* h, int32_t spec, int32_t lp, int32_t reps,
+                   double* ms);
+
+/* Cumulative kernel launches issued by the library: our own kernels and
+ * CUB primitive calls (radix sort / scan), graph replays included. */
+void imp_launch_count(unsigned long long* mine, unsigned long long* cub);
+
 #ifdef __cplusplus
 }
 #endif

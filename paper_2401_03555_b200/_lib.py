@@ -102,6 +102,11 @@ def _declare(lib):
     lib.imp_fp64_peak.argtypes = [c_i32, P_dbl]
     lib.imp_jit_compile.argtypes = [ctypes.POINTER(BuildDesc),
                                     ctypes.c_char_p]
+    lib.imp_time_sweep.argtypes = [c_vp, c_i32, c_i32, c_i32, P_dbl]
+    lib.imp_time_sweep.restype = c_i32
+    lib.imp_launch_count.argtypes = [ctypes.POINTER(ctypes.c_ulonglong),
+                                     ctypes.POINTER(ctypes.c_ulonglong)]
+    lib.imp_launch_count.restype = None
     for name in ("imp_device_query", "imp_imdp_import", "imp_imdp_info_get",
                  "imp_imdp_export", "imp_imdp_validate", "imp_build",
                  "imp_jit_compile",
@@ -115,7 +120,15 @@ EXPORTED = ("imp_last_error", "imp_version", "imp_device_query",
             "imp_imdp_validate", "imp_imdp_free", "imp_build",
             "imp_jit_compile",
             "imp_run_phase", "imp_bellman_step", "imp_row_values",
-            "imp_shard_sweep", "imp_fp64_peak")
+            "imp_shard_sweep", "imp_fp64_peak", "imp_time_sweep",
+            "imp_launch_count")
+
+
+def launch_count():
+    """(our kernels, CUB primitive calls) launched so far by the library."""
+    a, b = ctypes.c_ulonglong(0), ctypes.c_ulonglong(0)
+    load().imp_launch_count(ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
 
 
 def load(build_if_missing=True):

@@ -87,10 +87,27 @@ struct JitModule {
 std::mutex g_jit_mu;
 std::map<std::string, JitModule> g_jit_cache;
 
+// Threads per block of the NM kernels: the shared-memory simplex of every
+// thread ((N+1)*N + N+1 doubles) must fit in ~200 KB.
+int nm_block(int n) {
+  const size_t per = ((size_t)(n + 1) * n + (n + 1)) * sizeof(double);
+  int b = 128;
+  while (b > 32 && b * per > 200 * 1024) b /= 2;
+  return b;
+}
+
 std::string config_header(const imp_build_desc* d) {
   std::ostringstream o;
   o << "#define IMP_N " << d->n << "\n#define IMP_NC "
     << std::max(d->n_consts, 1) << "\n";
+  o << "#define IMP_MEAN_BLOCK " << nm_block(d->n) << "\n";
+  o << "#define IMP_REFINE_BLOCK " << nm_block(d->n) << "\n";
+  // tuning knobs (environment overrides for experiments)
+  const char* minb = getenv("IMPACT_REFINE_MINB");
+  o << "#define IMP_REFINE_MINB " << (minb ? atoi(minb) : (d->n <= 4 ? 4 : 2))
+    << "\n";
+  if (const char* ch = getenv("IMPACT_NDTR_CHUNK"))
+    o << "#define IMP_NDTR_CHUNK " << atoi(ch) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
   for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->n_deps[q];
   o << "};\n__device__ constexpr int kDeps[IMP_N][IMP_N] = {";
@@ -143,6 +160,12 @@ JitModule& jit(int device, const std::string& dyn_part) {
   std::lock_guard<std::mutex> lk(g_jit_mu);
   auto it = g_jit_cache.find(key);
   if (it != g_jit_cache.end()) return it->second;
+  if (getenv("IMPACT_DUMP_JIT")) {  // for ncu --import-source
+    if (FILE* f = fopen("impact_construct.cu", "w")) {
+      fwrite(src.data(), 1, src.size(), f);
+      fclose(f);
+    }
+  }
   std::vector<char> cubin = compile_cubin(src);
   IMP_CUDA(cudaSetDevice(device));
   IMP_CUDA(cudaFree(nullptr));  // bind the primary context
@@ -338,8 +361,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
 
     // --- stage 1: mean ranges -------------------------------------------------
     const size_t nm_doubles = (size_t)(N + 1) * N + (N + 1);
-    int block1 = 128;
-    while (block1 > 32 && block1 * nm_doubles * 8 > 96 * 1024) block1 -= 32;
+    const int block1 = nm_block(N);
     if (n_rows > 0) {
       const long long ntask = n_rows * N * 2;
       unsigned grid = (unsigned)std::min<long long>((ntask + block1 - 1) / block1,
@@ -386,7 +408,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     if (!d->separable && n_rows > 0) {
       P.n_items = nnz + naux + n_rows;
       instances = 2 * P.n_items;
-      const int block3 = 128;
+      const int block3 = nm_block(N);
       const size_t smem3 = block3 * nm_doubles * sizeof(double);
       const void* rfn = reinterpret_cast<const void*>(M.refine);
       if (smem3 > 48 * 1024)
@@ -441,6 +463,8 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     }
     h->row_ptr = std::move(row_ptr);
     finalize_imdp(h, s);
+    if (n_rows > 0)
+      count_launches(5 + (d->separable ? 0 : 1), 4);  // + slack kernel
     IMP_CUDA(cudaEventRecord(ev.e[5], s));
     IMP_CUDA(cudaEventSynchronize(ev.e[5]));
     if (stats) {

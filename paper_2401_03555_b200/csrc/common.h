@@ -106,4 +106,7 @@ struct imp_imdp {
 
 namespace imp {
 void finalize_imdp(imp_imdp* h, cudaStream_t s);  // slack + max_row
+// Kernel launches issued by this library (graph replays count every node):
+// our own kernels, and CUB primitive calls (sort / scan) separately.
+void count_launches(unsigned long long mine, unsigned long long cub);
 }

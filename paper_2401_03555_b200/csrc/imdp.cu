@@ -2,6 +2,7 @@
 // device facts and the FP64 roofline microbenchmark.
 #include <algorithm>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -11,6 +12,12 @@
 namespace imp {
 
 static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_mine{0}, g_cub{0};
+
+void count_launches(unsigned long long mine, unsigned long long cub) {
+  g_mine += mine;
+  g_cub += cub;
+}
 
 void set_error(const char* fmt, ...) {
   char buf[2048];
@@ -94,6 +101,12 @@ extern "C" size_t imp_last_error(char* buf, size_t len) {
 }
 
 extern "C" const char* imp_version(void) { return "impact_b200 0.1.0 sm_100a"; }
+
+extern "C" void imp_launch_count(unsigned long long* mine,
+                                 unsigned long long* cub) {
+  if (mine) *mine = g_mine.load();
+  if (cub) *cub = g_cub.load();
+}
 
 extern "C" int imp_device_query(int device, int* sm_count, int* cc_major,
                                 int* cc_minor) {

@@ -138,37 +138,47 @@ __device__ __forceinline__ void imp_start_point(const double* lo,
 // ---------------------------------------------------------------------------
 // Nelder-Mead (optimize.py:47-155) as a one-evaluation-per-step state
 // machine.  point() gives the next point to evaluate, feed() consumes its
-// objective value.  The simplex lives in shared memory (dynamic vertex
-// indexing, conflict-free stride = block size); centroid / candidates stay
-// in registers.
+// objective value.  Vertices live in shared memory in fixed physical slots
+// (conflict-free stride = block size); the sorted order is a packed 4-bit
+// permutation `ord` in a register, recomputed by a branch-free stable rank
+// (key = value, ties by current position -- numpy's stable argsort).  All
+// lanes that finish a step in any phase run the single iterate() site
+// together, so the bookkeeping does not serialise a warp per phase.
 // ---------------------------------------------------------------------------
 enum { NM_INIT = 0, NM_REFLECT = 1, NM_SECOND = 2, NM_SHRINK = 3 };
 enum { NM_EXPAND = 0, NM_OUTSIDE = 1, NM_INSIDE = 2 };
 
-template <int D>
+template <int D, int S>   // S: threads per block = shared-memory stride
 struct NelderMead {
-  double* X;   // X[(v * D + d) * S]
-  double* F;   // F[v * S]
-  int S;
+  static_assert(D + 1 <= 16, "4-bit permutation");
+  double* X;   // X[(slot * D + d) * S]
+  double* F;   // F[slot * S]
+  unsigned long long ord;
   double lo[D], hi[D];
   double c[D], xr[D], cand[D];
   double fr, tol, best;
   int phase, v, evals, kind, max_evals;
   bool done;
 
-  __device__ __forceinline__ double& x(int vv, int d) { return X[(vv * D + d) * S]; }
-  __device__ __forceinline__ double& f(int vv) { return F[vv * S]; }
+  __device__ __forceinline__ int slot(int q) const {
+    return (int)((ord >> (4 * q)) & 15ull);
+  }
+  __device__ __forceinline__ double& xs(int s, int d) { return X[(s * D + d) * S]; }
+  __device__ __forceinline__ double& fs(int s) { return F[s * S]; }
 
   __device__ void start(const double* s) {
+    ord = 0;
 #pragma unroll
-    for (int d = 0; d < D; ++d) x(0, d) = s[d];
+    for (int q = 0; q <= D; ++q) ord |= (unsigned long long)q << (4 * q);
+#pragma unroll
+    for (int d = 0; d < D; ++d) xs(0, d) = s[d];
 #pragma unroll
     for (int e = 0; e < D; ++e) {
       const double step = 0.25 * (hi[e] - lo[e]);
 #pragma unroll
-      for (int d = 0; d < D; ++d) x(e + 1, d) = s[d];
+      for (int d = 0; d < D; ++d) xs(e + 1, d) = s[d];
       const double up = s[e] + step;
-      x(e + 1, e) = up <= hi[e] ? up : s[e] - step;
+      xs(e + 1, e) = up <= hi[e] ? up : s[e] - step;
     }
     phase = NM_INIT;
     v = 0;
@@ -177,124 +187,112 @@ struct NelderMead {
   }
 
   __device__ __forceinline__ void point(double* p) {
-    if (phase == NM_REFLECT) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) p[d] = xr[d];
-    } else if (phase == NM_SECOND) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) p[d] = cand[d];
-    } else {
-#pragma unroll
-      for (int d = 0; d < D; ++d) p[d] = x(v, d);
-    }
-  }
-
-  __device__ void accept(const double* p, double fp) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) x(D, d) = p[d];
-    f(D) = fp;
-  }
-
-  __device__ void iterate() {
-    // stable insertion sort of the vertices by value
-    for (int i = 1; i <= D; ++i) {
-      for (int j = i; j > 0 && f(j) < f(j - 1); --j) {
-        double t = f(j);
-        f(j) = f(j - 1);
-        f(j - 1) = t;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          double u = x(j, d);
-          x(j, d) = x(j - 1, d);
-          x(j - 1, d) = u;
-        }
-      }
-    }
-    const double spread = f(D) - f(0);
-    if (!(spread > tol && evals < max_evals)) {
-      done = true;
-      best = f(0);
-      return;
-    }
+    const int sv = slot(v);
+    const bool vert = phase == NM_INIT || phase == NM_SHRINK;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      double s = x(0, d);
-      for (int vv = 1; vv < D; ++vv) s += x(vv, d);
+      double q = phase == NM_REFLECT ? xr[d] : cand[d];
+      if (vert) q = xs(sv, d);
+      p[d] = q;
+    }
+  }
+
+  // stable sort, termination test, centroid and reflection point
+  __device__ void iterate() {
+    double key[D + 1];
+    int sl[D + 1];
+#pragma unroll
+    for (int q = 0; q <= D; ++q) {
+      sl[q] = slot(q);
+      key[q] = fs(sl[q]);
+    }
+    unsigned long long nord = 0;
+#pragma unroll
+    for (int q = 0; q <= D; ++q) {
+      int rk = 0;
+#pragma unroll
+      for (int u = 0; u <= D; ++u)
+        rk += (key[u] < key[q]) || (u < q && key[u] == key[q]);
+      nord |= (unsigned long long)sl[q] << (4 * rk);
+    }
+    ord = nord;
+    const double f0 = fs(slot(0));
+    const double spread = fs(slot(D)) - f0;
+    if (!(spread > tol && evals < max_evals)) {
+      done = true;
+      best = f0;
+      return;
+    }
+    const int sw = slot(D);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      double s = xs(slot(0), d);
+#pragma unroll
+      for (int vv = 1; vv < D; ++vv) s += xs(slot(vv), d);
       c[d] = s / D;
-      xr[d] = imp_clip(c[d] + 1.0 * (c[d] - x(D, d)), lo[d], hi[d]);
+      xr[d] = imp_clip(c[d] + 1.0 * (c[d] - xs(sw, d)), lo[d], hi[d]);
     }
     phase = NM_REFLECT;
   }
 
   __device__ void feed(double fp) {
-    switch (phase) {
-      case NM_INIT:
-        f(v) = fp;
-        if (++v <= D) return;
-        evals = D + 1;
-        iterate();
-        return;
-      case NM_REFLECT: {
-        fr = fp;
-        evals += 1;
-        if (fr < f(0)) {
-          kind = NM_EXPAND;
-#pragma unroll
-          for (int d = 0; d < D; ++d)
-            cand[d] = imp_clip(c[d] + 2.0 * (c[d] - x(D, d)), lo[d], hi[d]);
-          phase = NM_SECOND;
-          return;
-        }
-        if (fr >= f(D - 1)) {
-          if (fr < f(D)) {
-            kind = NM_OUTSIDE;
-#pragma unroll
-            for (int d = 0; d < D; ++d)
-              cand[d] = imp_clip(c[d] + 0.5 * (xr[d] - c[d]), lo[d], hi[d]);
-          } else {
-            kind = NM_INSIDE;
-#pragma unroll
-            for (int d = 0; d < D; ++d)
-              cand[d] = imp_clip(c[d] + 0.5 * (x(D, d) - c[d]), lo[d], hi[d]);
-          }
-          phase = NM_SECOND;
-          return;
-        }
-        accept(xr, fr);
-        iterate();
-        return;
+    bool iter = false;
+    if (phase == NM_INIT || phase == NM_SHRINK) {
+      fs(slot(v)) = fp;
+      if (++v > D) {
+        evals += phase == NM_INIT ? D + 1 : D;
+        iter = true;
       }
-      case NM_SECOND: {
-        evals += 1;
-        if (kind == NM_EXPAND) {
-          if (fp < fr) accept(cand, fp);
-          else accept(xr, fr);
-          iterate();
-          return;
+    } else if (phase == NM_REFLECT) {
+      fr = fp;
+      evals += 1;
+      const double f0 = fs(slot(0)), fsw = fs(slot(D - 1)), fw = fs(slot(D));
+      const int sw = slot(D);
+      if (fr < f0 || fr >= fsw) {
+        kind = fr < f0 ? NM_EXPAND : (fr < fw ? NM_OUTSIDE : NM_INSIDE);
+        const double coef = kind == NM_EXPAND ? 2.0 : 0.5;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const double w = xs(sw, d);
+          const double dir = kind == NM_EXPAND ? c[d] - w
+                             : (kind == NM_OUTSIDE ? xr[d] - c[d] : w - c[d]);
+          cand[d] = imp_clip(c[d] + coef * dir, lo[d], hi[d]);
         }
-        if (kind == NM_OUTSIDE ? (fp < fr) : (fp < f(D))) {
-          accept(cand, fp);
-          iterate();
-          return;
-        }
+        phase = NM_SECOND;
+      } else {
+#pragma unroll
+        for (int d = 0; d < D; ++d) xs(sw, d) = xr[d];
+        fs(sw) = fr;
+        iter = true;
+      }
+    } else {  // NM_SECOND
+      evals += 1;
+      const int sw = slot(D);
+      const bool take = kind == NM_EXPAND ||
+                        (kind == NM_OUTSIDE ? fp < fr : fp < fs(sw));
+      if (take) {
+        const bool use_c = kind != NM_EXPAND || fp < fr;
+#pragma unroll
+        for (int d = 0; d < D; ++d) xs(sw, d) = use_c ? cand[d] : xr[d];
+        fs(sw) = use_c ? fp : fr;
+        iter = true;
+      } else {
+        const int s0 = slot(0);
+#pragma unroll
         for (int vv = 1; vv <= D; ++vv) {
+          const int sv = slot(vv);
 #pragma unroll
           for (int d = 0; d < D; ++d)
-            x(vv, d) = x(0, d) + 0.5 * (x(vv, d) - x(0, d));
+            xs(sv, d) = xs(s0, d) + 0.5 * (xs(sv, d) - xs(s0, d));
         }
         v = 1;
         phase = NM_SHRINK;
-        return;
       }
-      default:  // NM_SHRINK
-        f(v) = fp;
-        if (++v <= D) return;
-        evals += D;
-        iterate();
-        return;
     }
+    if (iter) iterate();
   }
 };
+
 
 __device__ __forceinline__ void imp_flag_nonfinite(const BuildParams& P,
                                                    long long row) {
@@ -322,10 +320,9 @@ __device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
     else P.mhi[r * IMP_N + DI] = v;
     return 0;
   } else {
-    NelderMead<D> nm;
+    NelderMead<D, IMP_MEAN_BLOCK> nm;
     nm.X = smem;
     nm.F = smem + (D + 1) * D * S;
-    nm.S = S;
     nm.tol = P.tol;
     nm.max_evals = imp_max_evals(P, D);
 #pragma unroll
@@ -374,9 +371,10 @@ __device__ __forceinline__ long long imp_mean_dispatch(int d,
   return 0;
 }
 
-extern "C" __global__ void k_mean_ranges(BuildParams P) {
+extern "C" __global__ void __launch_bounds__(IMP_MEAN_BLOCK)
+    k_mean_ranges(BuildParams P) {
   extern __shared__ double smem[];
-  const int S = blockDim.x;
+  constexpr int S = IMP_MEAN_BLOCK;
   const long long ntask = P.n_rows * IMP_N * 2;
   unsigned long long ev = 0;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -619,7 +617,9 @@ extern "C" __global__ void k_outer(BuildParams P) {
 // ---------------------------------------------------------------------------
 
 struct Instance {
-  long long row;
+  long long row, rel;          // row, item index within the row
+  long long nt, nx;            // live t entries / aux items of the row
+  long long t0, x0;            // CSR / aux offsets of the row
   int sgn;
   int kind;          // 0: t entry, 1: aux (target/avoid), 2: cover
   long long slot;    // CSR / aux index
@@ -628,51 +628,12 @@ struct Instance {
   const double* K;
 };
 
-__device__ void imp_setup_instance(const BuildParams& P, long long g,
-                                   Instance& I) {
-  const long long item = g >> 1;
-  I.sgn = (int)(g & 1);
-  // row = largest r with item_ptr[r] <= item, item_ptr = row_ptr + aux_ptr + r
-  long long lo = 0, hi = P.n_rows - 1;
-  while (lo < hi) {
-    const long long mid = (lo + hi + 1) >> 1;
-    if (P.row_ptr[mid] + P.aux_ptr[mid] + mid <= item) lo = mid;
-    else hi = mid - 1;
-  }
-  const long long r = lo;
-  I.row = r;
-  const long long rel = item - (P.row_ptr[r] + P.aux_ptr[r] + r);
-  const long long nt = P.row_ptr[r + 1] - P.row_ptr[r];
-  const long long nx = P.aux_ptr[r + 1] - P.aux_ptr[r];
-  int flat = -1;
-  if (rel < nt) {
-    I.kind = 0;
-    I.slot = P.row_ptr[r] + rel;
-    flat = P.safe_flat[P.col[I.slot]];
-  } else if (rel < nt + nx) {
-    I.kind = 1;
-    I.slot = P.aux_ptr[r] + (rel - nt);
-    const int code = P.aux_code[I.slot];
-    flat = code >= 0 ? P.target_flat[code] : P.avoid_flat[-1 - code];
-  } else {
-    I.kind = 2;
-    I.slot = r;
-  }
-  if (flat >= 0) {
-#pragma unroll
-    for (int d = 0; d < IMP_N; ++d) {
-      const int b = (flat / P.strides[d]) % P.counts[d];
-      const double* e = P.edges + P.edge_off[d];
-      I.blo[d] = e[b];
-      I.bhi[d] = e[b + 1];
-    }
-  } else {
-#pragma unroll
-    for (int d = 0; d < IMP_N; ++d) {
-      I.blo[d] = P.cover_lo[d];
-      I.bhi[d] = P.cover_hi[d];
-    }
-  }
+__device__ void imp_load_row(const BuildParams& P, Instance& I) {
+  const long long r = I.row;
+  I.t0 = P.row_ptr[r];
+  I.nt = P.row_ptr[r + 1] - I.t0;
+  I.x0 = P.aux_ptr[r];
+  I.nx = P.aux_ptr[r + 1] - I.x0;
   int k, j, i;
   imp_row_kji(P, r, k, j, i);
 #pragma unroll
@@ -683,16 +644,93 @@ __device__ void imp_setup_instance(const BuildParams& P, long long g,
   I.K = P.consts + (long long)(j * P.n_w + i) * IMP_NC;
 }
 
+__device__ void imp_load_item(const BuildParams& P, Instance& I) {
+  int flat = -1;
+  if (I.rel < I.nt) {
+    I.kind = 0;
+    I.slot = I.t0 + I.rel;
+    flat = P.safe_flat[P.col[I.slot]];
+  } else if (I.rel < I.nt + I.nx) {
+    I.kind = 1;
+    I.slot = I.x0 + (I.rel - I.nt);
+    const int code = P.aux_code[I.slot];
+    flat = code >= 0 ? P.target_flat[code] : P.avoid_flat[-1 - code];
+  } else {
+    I.kind = 2;
+    I.slot = I.row;
+  }
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) {
+    double lo = P.cover_lo[d], hi = P.cover_hi[d];
+    if (flat >= 0) {
+      const int b = (flat / P.strides[d]) % P.counts[d];
+      const double* e = P.edges + P.edge_off[d];
+      lo = e[b];
+      hi = e[b + 1];
+    }
+    I.blo[d] = lo;
+    I.bhi[d] = hi;
+  }
+}
+
+// Instance g = 2 * item + sign; items of row r are its live t entries, then
+// its live target / avoid boxes, then the cover box.
+__device__ void imp_seek_instance(const BuildParams& P, long long g,
+                                  Instance& I) {
+  const long long item = g >> 1;
+  I.sgn = (int)(g & 1);
+  long long lo = 0, hi = P.n_rows - 1;
+  while (lo < hi) {   // last row with item_ptr[row] <= item
+    const long long mid = (lo + hi + 1) >> 1;
+    if (P.row_ptr[mid] + P.aux_ptr[mid] + mid <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  I.row = lo;
+  imp_load_row(P, I);
+  I.rel = item - (I.t0 + I.x0 + I.row);
+  imp_load_item(P, I);
+}
+
+__device__ void imp_next_instance(const BuildParams& P, Instance& I) {
+  if (I.sgn == 0) {          // same box, max side
+    I.sgn = 1;
+    return;
+  }
+  I.sgn = 0;
+  if (++I.rel == I.nt + I.nx + 1) {
+    ++I.row;
+    I.rel = 0;
+    imp_load_row(P, I);
+  }
+  imp_load_item(P, I);
+}
+
 // P(f(x) + noise in box) * sign  (abstraction.py:333-349)
 __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
                                                     const Instance& I,
                                                     const double* x) {
-  double prob = 1.0;
+  // all 2N normal CDFs of one evaluation in one branch-free batch
+  double arg[2 * IMP_N], cdf[2 * IMP_N], mean[IMP_N];
+  imp_f_all(x, I.K, mean);
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) {
-    const double m = imp_fd(d, x, I.K);
-    prob *= imp_interval_prob(P.sigma[d], m, I.blo[d], I.bhi[d]);
+    const double m = mean[d];
+    const double s = P.sigma[d];
+    arg[2 * d] = (I.bhi[d] - m) / s;
+    arg[2 * d + 1] = (I.blo[d] - m) / s;
   }
+#ifndef IMP_NDTR_CHUNK
+#define IMP_NDTR_CHUNK 1
+#endif
+#if IMP_NDTR_CHUNK == 0
+#pragma unroll 1
+  for (int j = 0; j < 2 * IMP_N; ++j) cdf[j] = imp_ndtr(arg[j]);
+#else
+  imp_ndtr_chunks<2 * IMP_N, IMP_NDTR_CHUNK>(arg, cdf);
+#endif
+  double prob = 1.0;
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) prob *= cdf[2 * d] - cdf[2 * d + 1];
   return I.sgn ? prob * -1.0 : prob;
 }
 
@@ -713,22 +751,28 @@ __device__ void imp_store_instance(const BuildParams& P, const Instance& I,
   }
 }
 
-extern "C" __global__ void __launch_bounds__(128) k_refine(BuildParams P) {
+// Every thread owns a contiguous run of instances (balanced by count; NM
+// costs average out over thousands of instances per thread), found once by
+// binary search and then advanced incrementally.
+extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
+    k_refine(BuildParams P) {
   extern __shared__ double smem[];
-  const int S = blockDim.x;
-  NelderMead<IMP_N> nm;
+  constexpr int S = IMP_REFINE_BLOCK;
+  NelderMead<IMP_N, S> nm;
   nm.X = smem + threadIdx.x;
   nm.F = smem + (IMP_N + 1) * IMP_N * S + threadIdx.x;
-  nm.S = S;
   nm.tol = P.tol;
   nm.max_evals = imp_max_evals(P, IMP_N);
   const int ms = imp_multistart(P, IMP_N);
   const long long total = 2 * P.n_items;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= total) return;
+  const long long nthreads = (long long)gridDim.x * blockDim.x;
+  const long long chunk = (total + nthreads - 1) / nthreads;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long g = tid * chunk;
+  const long long g_end = min(total, g + chunk);
+  if (g >= g_end) return;
   Instance I;
-  imp_setup_instance(P, g, I);
+  imp_seek_instance(P, g, I);
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) {
     nm.lo[d] = I.clo[d];
@@ -742,37 +786,50 @@ extern "C" __global__ void __launch_bounds__(128) k_refine(BuildParams P) {
     imp_start_point<IMP_N>(nm.lo, nm.hi, 0, st);
     nm.start(st);
   }
-  for (;;) {
-    double p[IMP_N];
-    nm.point(p);
-    double val = imp_box_objective(P, I, p);
-    if (!imp_finite(val)) {
-      imp_flag_nonfinite(P, I.row);
-      val = 0.0;
-    }
-    ++ev;
-    nm.feed(val);
-    if (!nm.done) continue;
-    best = fmin(best, nm.best);
-    if (++s == ms) {
-      imp_store_instance(P, I, best);
-      g += stride;
-      if (g >= total) break;
-      imp_setup_instance(P, g, I);
-#pragma unroll
-      for (int d = 0; d < IMP_N; ++d) {
-        nm.lo[d] = I.clo[d];
-        nm.hi[d] = I.chi[d];
+  // One objective evaluation per trip for every live lane; the restart path
+  // is a nested branch that reconverges before the next evaluation, so a
+  // warp never splits into groups evaluating the objective separately.
+  bool live = true;
+  while (__any_sync(__activemask(), live)) {
+    if (live) {
+      double p[IMP_N];
+      nm.point(p);
+      double val = imp_box_objective(P, I, p);
+      if (!imp_finite(val)) {
+        imp_flag_nonfinite(P, I.row);
+        val = 0.0;
       }
-      s = 0;
-      best = IMP_INF;
+      ++ev;
+      nm.feed(val);
+      if (nm.done) {
+        best = fmin(best, nm.best);
+        if (++s == ms) {
+          imp_store_instance(P, I, best);
+          if (++g >= g_end) {
+            live = false;
+          } else {
+            imp_next_instance(P, I);
+#pragma unroll
+            for (int d = 0; d < IMP_N; ++d) {
+              nm.lo[d] = I.clo[d];
+              nm.hi[d] = I.chi[d];
+            }
+            s = 0;
+            best = IMP_INF;
+          }
+        }
+        if (live) {
+          double st[IMP_N];
+          imp_start_point<IMP_N>(nm.lo, nm.hi, s, st);
+          nm.start(st);
+        }
+      }
     }
-    double st[IMP_N];
-    imp_start_point<IMP_N>(nm.lo, nm.hi, s, st);
-    nm.start(st);
+    __syncwarp(__activemask());
   }
   atomicAdd((unsigned long long*)P.evals, ev);
 }
+
 
 // ---------------------------------------------------------------------------
 // Stage 4: assemble (abstraction.py:607-659), one warp per row

@@ -535,6 +535,7 @@ struct Work {
   DevBuf<unsigned char> cub_tmp;
   DevBuf<Ctl> ctl;
   size_t cub_bytes = 0;
+  SweepArgs last_sweep{};   // arguments of the last enqueued K5 launch
 
   void init(const imp_imdp* h, int64_t phase_rows) {
     n_s = h->n_s;
@@ -626,8 +627,9 @@ struct Launch {
 };
 
 // Enqueue one iteration: order keys, 2 stable sorts, ranks, sweep, reduce
-// (+ control when use_ctl).
-void enqueue_iteration(const Launch& L, cudaStream_t s) {
+// (+ control when use_ctl).  Returns the number of our own kernels
+// enqueued (the two CUB sorts come on top).
+int enqueue_iteration(const Launch& L, cudaStream_t s) {
   const imp_imdp* h = L.h;
   Work& w = *L.w;
   Ctl* ctl = L.use_ctl ? w.ctl.ptr : nullptr;
@@ -700,6 +702,7 @@ void enqueue_iteration(const Launch& L, cudaStream_t s) {
   if (tm.team == 0) fail(IMP_E_ARG, "row longer than 16384 stored entries");
   if (w.wide) launch_sweep_w<true>(sa, tm, L.sms, s);
   else launch_sweep_w<false>(sa, tm, L.sms, s);
+  w.last_sweep = sa;
 
   ReduceArgs rd{};
   rd.ctl = ctl;
@@ -726,6 +729,7 @@ void enqueue_iteration(const Launch& L, cudaStream_t s) {
     k_control<<<1, 1, 0, s>>>(ctl);
     IMP_CUDA(cudaGetLastError());
   }
+  return 3 + (w.wide ? 0 : 1) + (h->k_count > 0 ? 1 : 0) + (ctl ? 1 : 0);
 }
 
 __global__ void k_fill(double* p, int64_t n, double v) {
@@ -798,7 +802,8 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     IMP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    for (int g = 0; g < G; ++g) enqueue_iteration(L, s);
+    int per_graph = 0;
+    for (int g = 0; g < G; ++g) per_graph += enqueue_iteration(L, s);
     IMP_CUDA(cudaStreamEndCapture(s, &graph));
     IMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     struct GraphGuard {
@@ -814,6 +819,7 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     Ctl hc{};
     for (;;) {
       IMP_CUDA(cudaGraphLaunch(exec, s));
+      count_launches(per_graph, 2 * G);
       IMP_CUDA(cudaMemcpyAsync(&hc, w.ctl.ptr, sizeof(Ctl),
                                cudaMemcpyDeviceToHost, s));
       IMP_CUDA(cudaStreamSynchronize(s));
@@ -884,7 +890,7 @@ void explicit_step(imp_imdp* h, const double* v0, const double* v1, int spec,
   L.new_explicit[1] = new1;
   L.stats_explicit = stats;
   L.use_ctl = false;
-  enqueue_iteration(L, s);
+  count_launches(enqueue_iteration(L, s), 2);
   if (policy_dev)
     IMP_CUDA(cudaMemcpyAsync(policy_dev, w.policy.ptr,
                              sizeof(int64_t) * h->k_count,
@@ -1026,5 +1032,65 @@ extern "C" int imp_row_values(imp_imdp* h, const double* weights, int32_t lp,
     IMP_CUDA(cudaMemcpy(out, w.val[0].ptr, sizeof(double) * h->n_rows,
                         on_device ? cudaMemcpyDeviceToDevice
                                   : cudaMemcpyDeviceToHost));
+  });
+}
+
+// K5 alone, for the HBM roofline: one iteration sets up the orders for a
+// scrambled value vector, then `reps` twin sweeps over every phase-1 row are
+// timed with CUDA events on the launching stream.  *ms = mean per sweep.
+extern "C" int imp_time_sweep(imp_imdp* h, int32_t spec, int32_t lp,
+                              int32_t reps, double* ms) {
+  return guarded([&] {
+    IMP_REQUIRE(h && ms && reps > 0, "bad argument");
+    IMP_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s;
+    IMP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+    std::vector<double> hv(h->n_s);
+    for (int c = 0; c < h->n_s; ++c) {
+      double f = c * 0.6180339887498949;
+      hv[c] = f - std::floor(f);
+    }
+    DevBuf<double> v0(h->n_s), v1(h->n_s), n0(std::max(h->k_count, 1)),
+        n1(std::max(h->k_count, 1)), st(4);
+    IMP_CUDA(cudaMemcpy(v0.ptr, hv.data(), sizeof(double) * h->n_s,
+                        cudaMemcpyHostToDevice));
+    for (auto& x : hv) x = 1.0 - x;
+    IMP_CUDA(cudaMemcpy(v1.ptr, hv.data(), sizeof(double) * h->n_s,
+                        cudaMemcpyHostToDevice));
+    Work w;
+    w.init(h, h->n_rows);
+    Launch L{};
+    L.h = h;
+    L.w = &w;
+    L.sms = sm_count_of(h->device);
+    L.spec = spec;
+    L.lp = lp;
+    L.u_max = spec == IMP_SPEC_REACH;
+    L.v_explicit[0] = v0.ptr;
+    L.v_explicit[1] = v1.ptr;
+    L.new_explicit[0] = n0.ptr;
+    L.new_explicit[1] = n1.ptr;
+    L.stats_explicit = st.ptr;
+    L.use_ctl = false;
+    enqueue_iteration(L, s);
+    const SweepArgs sa = w.last_sweep;
+    const Team tm = choose_team(h->max_row);
+    cudaEvent_t e0, e1;
+    IMP_CUDA(cudaEventCreate(&e0));
+    IMP_CUDA(cudaEventCreate(&e1));
+    IMP_CUDA(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r) {
+      if (w.wide) launch_sweep_w<true>(sa, tm, L.sms, s);
+      else launch_sweep_w<false>(sa, tm, L.sms, s);
+    }
+    IMP_CUDA(cudaEventRecord(e1, s));
+    IMP_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    count_launches(reps, 0);
+    *ms = t / reps;
   });
 }

@@ -378,11 +378,20 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
     """Fold every x-free subtree on the host (numpy, reference evaluation
     order) and emit the x-dependent residual as CUDA C."""
     folded = []          # list of subtree nodes, index = constant slot
+    slot_of = {}
+
+    def fold(node):
+        if node not in slot_of:
+            slot_of[node] = len(folded)
+            folded.append(node)
+        return f"k[{slot_of[node]}]"
+
+    def xfree(node):
+        return not any(v.startswith("x") for v in _vars(node, set()))
 
     def emit(node):
-        if not any(v.startswith("x") for v in _vars(node, set())):
-            folded.append(node)
-            return f"k[{len(folded) - 1}]"
+        if xfree(node):
+            return fold(node)
         tag = node[0]
         if tag == "var":
             return f"x[{int(node[1][1:]) - 1}]"
@@ -409,6 +418,7 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
     for d in range(n):
         lines.append(f"    case {d}: return imp_f{d}(x, k);")
     lines.append("  }\n  return 0.0;\n}")
+    lines += _emit_all(dyn, fold, xfree)
     src = "\n".join(lines) + "\n"
 
     n_u, n_w = len(input_reps), len(disturb_reps)
@@ -424,6 +434,75 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
     deps = [sorted(dyn.state_dependencies(d)) for d in range(n)]
     return LoweredDynamics(source=src, n_consts=len(folded), consts=consts,
                            deps=deps)
+
+
+def _emit_all(dyn, fold, xfree):
+    """imp_f_all(x, k, f): every f_d at once, identical x-dependent
+    subtrees computed once (common-subexpression elimination) and sin/cos
+    of one argument fused into sincos().  Evaluation order and rounding of
+    each subtree are unchanged, so values equal imp_f<d>'s."""
+    from collections import Counter
+    seen = Counter()
+
+    def count(node):
+        if xfree(node) or node[0] == "var":
+            return
+        seen[node] += 1
+        if seen[node] > 1:
+            return
+        kids = {"neg": lambda n: [n[1]], "bin": lambda n: [n[2], n[3]],
+                "call": lambda n: list(n[2])}[node[0]](node)
+        for c in kids:
+            count(c)
+
+    for e in dyn.exprs:
+        count(e.node)
+    trig_args = {}
+    for node in seen:
+        if node[0] == "call" and node[1] in ("sin", "cos"):
+            trig_args.setdefault(node[2][0], set()).add(node[1])
+    paired = {a for a, fns in trig_args.items() if fns == {"sin", "cos"}}
+    body, memo, sc = [], {}, {}
+
+    def gen(node):
+        if xfree(node):
+            return fold(node)
+        if node in memo:
+            return memo[node]
+        tag = node[0]
+        if tag == "var":
+            return f"x[{int(node[1][1:]) - 1}]"
+        if tag == "call" and node[1] in ("sin", "cos") and node[2][0] in paired:
+            arg = node[2][0]
+            if arg not in sc:
+                a = gen(arg)
+                q = len(sc)
+                body.append(f"  double s{q}, c{q};\n  sincos({a}, &s{q}, &c{q});")
+                sc[arg] = q
+            name = f"{'s' if node[1] == 'sin' else 'c'}{sc[arg]}"
+            memo[node] = name
+            return name
+        if tag == "neg":
+            s = f"(-{gen(node[1])})"
+        elif tag == "bin":
+            a, b = gen(node[2]), gen(node[3])
+            s = f"pow({a}, {b})" if node[1] == "^" else f"({a} {node[1]} {b})"
+        else:
+            s = f"{_CUDA_FN[node[1]]}({', '.join(gen(a) for a in node[2])})"
+        if seen[node] > 1 or tag == "call":
+            t = f"t{len(memo)}"
+            body.append(f"  const double {t} = {s};")
+            memo[node] = t
+            return t
+        return s
+
+    outs = [gen(e.node) for e in dyn.exprs]
+    lines = ["__device__ __forceinline__ void imp_f_all(const double* x, "
+             "const double* k, double* f) {"]
+    lines += body
+    lines += [f"  f[{d}] = {o};" for d, o in enumerate(outs)]
+    lines.append("}")
+    return lines
 
 
 def has_x_transcendental(dyn: DynamicsSpec) -> bool:
