@@ -215,8 +215,9 @@ int imp_row_values(imp_imdp* h, const double* weights, int32_t lp,
  * (device pointers, n_s each): writes this shard's new values to
  * new0/new1 (device, k_count each), chosen inputs to policy (device,
  * k_count) and the shard's max |dV0|, max |dV1|, max(v1'-v0') and the
- * monotone/bracket flags to stats[0..4] (device doubles).  stream is a
- * cudaStream_t (NULL = legacy default). */
+ * monotone/bracket flags (0/1) to stats[0..4] (5 device doubles; an empty
+ * shard reports -inf maxima).  stream is a cudaStream_t (NULL = legacy
+ * default); the call returns after the stream work completed. */
 int imp_shard_sweep(imp_imdp* h, const double* v0, const double* v1,
                     int32_t spec, int32_t lp, int32_t u_max,
                     const int64_t* fixed_policy_dev, double* new0,

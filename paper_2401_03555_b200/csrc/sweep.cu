@@ -867,6 +867,38 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
 
 namespace imp {
 namespace {
+// Explicit-mode stats (order_key-encoded maxima + flag bits) -> plain
+// doubles [max|dV0|, max|dV1|, max(V1'-V0'), monotone, bracket]; an empty
+// shard reports -inf maxima (neutral under a max all-reduce).
+__global__ void k_decode_stats(double* st) {
+  unsigned long long* u = reinterpret_cast<unsigned long long*>(st);
+  const unsigned flags = *reinterpret_cast<unsigned*>(u + 3);
+  double v[3];
+  for (int q = 0; q < 3; ++q) v[q] = u[q] ? key_value(u[q]) : -INFINITY;
+  st[0] = v[0];
+  st[1] = v[1];
+  st[2] = v[2];
+  st[3] = (flags & 1u) ? 1.0 : 0.0;
+  st[4] = (flags & 2u) ? 1.0 : 0.0;
+}
+
+void free_work(void* p) { delete static_cast<Work*>(p); }
+
+// Per-handle cached working set for host-driven iterations (sharded loop):
+// reallocated only when the phase row count changes.
+Work& cached_work(imp_imdp* h, int64_t phase_rows) {
+  Work* w = static_cast<Work*>(h->sweep_cache);
+  if (!w || h->sweep_cache_rows != phase_rows) {
+    delete w;
+    w = new Work();
+    w->init(h, phase_rows);
+    h->sweep_cache = w;
+    h->sweep_cache_rows = phase_rows;
+    h->free_cache = free_work;
+  }
+  return *w;
+}
+
 // Shared body of the explicit (host-driven) single iterations.
 void explicit_step(imp_imdp* h, const double* v0, const double* v1, int spec,
                    int lp, int u_max, const int64_t* fixed_dev, double* new0,
@@ -874,8 +906,7 @@ void explicit_step(imp_imdp* h, const double* v0, const double* v1, int spec,
                    cudaStream_t s) {
   const int64_t phase_rows = fixed_dev ? (int64_t)h->k_count * h->n_w
                                        : h->n_rows;
-  Work w;
-  w.init(h, phase_rows);
+  Work& w = cached_work(h, phase_rows);
   Launch L{};
   L.h = h;
   L.w = &w;
@@ -891,6 +922,11 @@ void explicit_step(imp_imdp* h, const double* v0, const double* v1, int spec,
   L.stats_explicit = stats;
   L.use_ctl = false;
   count_launches(enqueue_iteration(L, s), 2);
+  if (stats) {
+    k_decode_stats<<<1, 1, 0, s>>>(stats);
+    IMP_CUDA(cudaGetLastError());
+    count_launches(1, 0);
+  }
   if (policy_dev)
     IMP_CUDA(cudaMemcpyAsync(policy_dev, w.policy.ptr,
                              sizeof(int64_t) * h->k_count,
@@ -938,7 +974,7 @@ extern "C" int imp_shard_sweep(imp_imdp* h, const double* v0,
     IMP_REQUIRE(h && v0 && v1 && new0 && new1 && stats, "null argument");
     IMP_CUDA(cudaSetDevice(h->device));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    IMP_CUDA(cudaMemsetAsync(stats, 0, 4 * sizeof(double), s));
+    IMP_CUDA(cudaMemsetAsync(stats, 0, 5 * sizeof(double), s));
     explicit_step(h, v0, v1, spec, lp, u_max, fixed_dev, new0, new1, policy,
                   stats, s);
   });
