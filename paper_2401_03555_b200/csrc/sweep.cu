@@ -48,11 +48,13 @@ __device__ __forceinline__ double key_value(uint64_t k) {
   return __longlong_as_double((long long)u);
 }
 
-// Deterministic warp sum: fixed shfl_down tree, lane 0's result broadcast.
+// Deterministic warp sum: xor butterfly.  Partners add the same two
+// operands (a + b == b + a in IEEE), so after five steps every lane holds
+// the bit-identical total, with no broadcast.
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
-  return __shfl_sync(FULL, v, 0);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
 }
 
 // Control block of a phase loop living in device memory.  Kernels of an
@@ -164,6 +166,13 @@ struct SweepArgs {
   const int64_t* fixed;     // phase-2 policy (local states) or nullptr
   int64_t n_phase_rows;
   int n_u, n_w, n_s, n, nbits;
+  // row class handled by this launch (fixed thresholds on the row's own
+  // stored length m, so the kernel -- hence the summation tree -- a row
+  // gets never depends on its shard or neighbours)
+  int m_lo, m_hi;       // m_lo < m <= m_hi
+  int dense_sel;        // 1: rows of the rank-space class, 0: the others
+  int dense_ok;         // rank-space kernel usable for this n
+  int* hint;            // (2 * n_phase_rows) warm-start crossing entries
   double* out0;
   double* out1;
 };
@@ -192,6 +201,11 @@ struct RankReg<true> {
   }
   __device__ __forceinline__ void none() { x = y = 0x7fffffff; }
 };
+
+__device__ __forceinline__ bool row_in_class(const SweepArgs& a, int m) {
+  const bool dense = a.dense_ok && 4 * m >= a.n_s;
+  return dense == (a.dense_sel != 0) && m > a.m_lo && m <= a.m_hi;
+}
 
 __device__ __forceinline__ int64_t phase_row(const SweepArgs& a, int64_t t) {
   if (!a.fixed) return t;
@@ -222,7 +236,16 @@ __device__ __forceinline__ double2 team_sum2(double x, double y,
 }
 
 // One row per team.  TEAM threads hold up to TEAM*EPT stored entries in
-// registers; the two virtual slots (target, avoid) live in team thread 0.
+// registers (missing entries padded with h = 0, rank = +inf, so every loop
+// is unguarded and the per-lane sums do not depend on EPT); the two
+// virtual slots (target, avoid) live in team thread 0.
+//
+// Warm start: `hint` keeps, per phase row and track, the row-local index of
+// last sweep's crossing entry (-1: no crossing, -2: unknown).  Near
+// convergence the global order barely moves, so the guess usually verifies
+// with one two-sided probe; otherwise the binary search runs.  Either way
+// the value is computed from C(<P*) with the same reduction, so the result
+// is independent of the hint (bitwise).
 template <int TEAM, int EPT, bool WIDE>
 __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
     k_sweep(SweepArgs a) {
@@ -240,7 +263,7 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
     const int64_t row = phase_row(a, t);
     const int64_t beg = a.row_ptr[row];
     const int m = (int)(a.row_ptr[row + 1] - beg);
-    const int nch = (m + TEAM - 1) / TEAM;   // team-uniform
+    if (!row_in_class(a, m)) continue;
 
     double h[EPT];
     RankReg<WIDE> rk[EPT];
@@ -249,18 +272,16 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
     for (int e = 0; e < EPT; ++e) {
       h[e] = 0.0;
       rk[e].none();
-      if (e < nch) {
-        int q = e * TEAM + tid;
-        if (q < m) {
-          int c = __ldg(a.col + beg + q);
-          double l = __ldg(a.lo + beg + q);
-          double u = __ldg(a.hi + beg + q);
-          h[e] = u - l;
-          double2 w = __ldg(a.colw + c);
-          lw0 += l * w.x;
-          lw1 += l * w.y;
-          rk[e].load(a, c);
-        }
+      const int q = e * TEAM + tid;
+      if (q < m) {
+        const int c = __ldg(a.col + beg + q);
+        const double l = __ldg(a.lo + beg + q);
+        const double u = __ldg(a.hi + beg + q);
+        h[e] = u - l;
+        const double2 w = __ldg(a.colw + c);
+        lw0 += l * w.x;
+        lw1 += l * w.y;
+        rk[e].load(a, c);
       }
     }
     // virtual slots n_s (target) and n_s + 1 (avoid) on team thread 0
@@ -269,10 +290,10 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
     rv[0].none();
     rv[1].none();
     if (tid == 0) {
-      double lr = a.r_min[row], la = a.a_min[row];
+      const double lr = a.r_min[row], la = a.a_min[row];
       hv[0] = a.r_max[row] - lr;
       hv[1] = a.a_max[row] - la;
-      double2 wr = __ldg(a.colw + a.n_s), wa = __ldg(a.colw + a.n_s + 1);
+      const double2 wr = __ldg(a.colw + a.n_s), wa = __ldg(a.colw + a.n_s + 1);
       lw0 += lr * wr.x + la * wa.x;
       lw1 += lr * wr.y + la * wa.y;
       rv[0].load(a, a.n_s);
@@ -280,18 +301,13 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
     }
     const double s = a.slack[row];
 
-    // binary search for P (largest rank with C(<P) < slack), both tracks
-    int p0 = 0, p1 = 0;
-    double c0 = 0.0, c1 = 0.0;
-    for (int b = a.nbits - 1; b >= 0; --b) {
-      const int q0 = p0 + (1 << b), q1 = p1 + (1 << b);
+    // C(<q) for both tracks: the one reduction every decision is based on
+    auto below = [&](int q0, int q1) {
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int e = 0; e < EPT; ++e) {
-        if (e < nch) {
-          if (rk[e].r0() < q0) s0 += h[e];
-          if (rk[e].r1() < q1) s1 += h[e];
-        }
+        if (rk[e].r0() < q0) s0 += h[e];
+        if (rk[e].r1() < q1) s1 += h[e];
       }
       if (tid == 0) {
 #pragma unroll
@@ -300,30 +316,86 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
           if (rv[v].r1() < q1) s1 += hv[v];
         }
       }
-      double2 tot = team_sum2<TEAM>(s0, s1, part, parity);
-      if (q0 <= a.n && tot.x < s) { p0 = q0; c0 = tot.x; }
-      if (q1 <= a.n && tot.y < s) { p1 = q1; c1 = tot.y; }
+      return team_sum2<TEAM>(s0, s1, part, parity);
+    };
+
+    // warm start: rank of last sweep's crossing entry
+    int g0 = -2, g1 = -2;
+    if (a.hint) {
+      const int hq[2] = {a.hint[2 * t], a.hint[2 * t + 1]};
+      int gr[2];
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        gr[o] = hq[o];
+        if (hq[o] >= 0) {
+          const int c = hq[o] < m ? __ldg(a.col + beg + hq[o])
+                                  : a.n_s + (hq[o] - m);
+          RankReg<WIDE> r;
+          r.load(a, c);
+          gr[o] = o ? r.r1() : r.r0();
+        } else if (hq[o] == -1) {
+          gr[o] = a.n;          // "no crossing": verify C(<n) < s
+        }
+      }
+      g0 = gr[0];
+      g1 = gr[1];
+    }
+    int p0 = 0, p1 = 0;
+    double c0 = 0.0, c1 = 0.0;
+    // zero slack: nothing is filled, P = 0 with C = 0 (what the search gives)
+    bool ok0 = !(s > 0.0), ok1 = !(s > 0.0);
+    if (!ok0 && (g0 >= 0 || g1 >= 0)) {
+      const int a0 = g0 >= 0 ? g0 : 0, a1 = g1 >= 0 ? g1 : 0;
+      const double2 lt = below(a0, a1);
+      const double2 le = below(a0 + 1, a1 + 1);
+      ok0 = g0 >= 0 && lt.x < s && (g0 == a.n || le.x >= s);
+      ok1 = g1 >= 0 && lt.y < s && (g1 == a.n || le.y >= s);
+      if (ok0) { p0 = g0; c0 = lt.x; }
+      if (ok1) { p1 = g1; c1 = lt.y; }
+    }
+    if (!(ok0 && ok1)) {
+      // binary search for P (largest rank with C(<P) < slack)
+      int b0 = 0, b1 = 0;
+      double d0 = 0.0, d1 = 0.0;
+      for (int b = a.nbits - 1; b >= 0; --b) {
+        const int q0 = b0 + (1 << b), q1 = b1 + (1 << b);
+        const double2 tot = below(q0, q1);
+        if (q0 <= a.n && tot.x < s) { b0 = q0; d0 = tot.x; }
+        if (q1 <= a.n && tot.y < s) { b1 = q1; d1 = tot.y; }
+      }
+      if (!ok0) { p0 = b0; c0 = d0; }
+      if (!ok1) { p1 = b1; c1 = d1; }
     }
     // filled part: sum_{rank<P} head * w, weights regathered by rank
-    double g0 = 0.0, g1 = 0.0;
+    double f0 = 0.0, f1 = 0.0;
+    int e0 = -1, e1 = -1;   // row-local index of the crossing entry
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
-      if (e < nch) {
-        int r0 = rk[e].r0(), r1 = rk[e].r1();
-        if (r0 < p0) g0 += h[e] * __ldg(a.ws0 + r0);
-        if (r1 < p1) g1 += h[e] * __ldg(a.ws1 + r1);
-      }
+      const int r0 = rk[e].r0(), r1 = rk[e].r1();
+      if (r0 < p0) f0 += h[e] * __ldg(a.ws0 + r0);
+      if (r1 < p1) f1 += h[e] * __ldg(a.ws1 + r1);
+      if (r0 == p0) e0 = e * TEAM + tid;
+      if (r1 == p1) e1 = e * TEAM + tid;
     }
     if (tid == 0) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        int r0 = rv[v].r0(), r1 = rv[v].r1();
-        if (r0 < p0) g0 += hv[v] * __ldg(a.ws0 + r0);
-        if (r1 < p1) g1 += hv[v] * __ldg(a.ws1 + r1);
+        const int r0 = rv[v].r0(), r1 = rv[v].r1();
+        if (r0 < p0) f0 += hv[v] * __ldg(a.ws0 + r0);
+        if (r1 < p1) f1 += hv[v] * __ldg(a.ws1 + r1);
+        if (r0 == p0) e0 = m + v;
+        if (r1 == p1) e1 = m + v;
       }
     }
-    double2 lw = team_sum2<TEAM>(lw0, lw1, part, parity);
-    double2 g = team_sum2<TEAM>(g0, g1, part, parity);
+    const double2 lw = team_sum2<TEAM>(lw0, lw1, part, parity);
+    const double2 g = team_sum2<TEAM>(f0, f1, part, parity);
+    if (a.hint) {
+      // publish the crossing entries (exactly one thread holds each)
+      if (p0 >= a.n && tid == 0) a.hint[2 * t] = -1;
+      else if (e0 >= 0) a.hint[2 * t] = e0;
+      if (p1 >= a.n && tid == 0) a.hint[2 * t + 1] = -1;
+      else if (e1 >= 0) a.hint[2 * t + 1] = e1;
+    }
     if (tid == 0) {
       double x0 = g.x, x1 = g.y;
       if (p0 < a.n) x0 += (s - c0) * a.ws0[p0];
@@ -331,6 +403,199 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
       a.out0[t] = lw.x + x0;
       a.out1[t] = lw.y + x1;
     }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// K5 variant for wide rows (live entries a large fraction of the columns:
+// vehicle3d, dim14).  Rank-space form of the same greedy fill: a CTA
+// scatters the row's headroom into a dense shared-memory vector indexed by
+// global rank, then scans it in rank order -- O(n) shared-memory work per
+// row instead of log2(n) team reductions, no binary search.
+//   pass 1  every warp totals sum(h) and sum(h * w_sorted) over a fixed
+//           contiguous block of ranks (coalesced chunks of 32);
+//   scan    block exclusive scan of the warp totals (fixed tree) locates
+//           the warp whose block holds the crossing;
+//   pass 2  that warp walks its block chunk by chunk (warp inclusive scan)
+//           to the crossing rank P and its partial sums;
+// value = sum(l*w) + sum_{rank<P} h w + (slack - C(<P)) w_sorted[P].
+// The partition of ranks into warps / chunks / lanes depends only on n, so
+// results depend only on the row's contents (position independent).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+template <int T, int EPT, bool WIDE>
+__global__ void __launch_bounds__(T) k_sweep_dense(SweepArgs a) {
+  if (a.ctl && a.ctl->done) return;
+  extern __shared__ double hs[];            // (n) headroom by rank
+  __shared__ double wtot[2][T / 32];        // per-warp sum(h), sum(h w)
+  __shared__ int cross_w;
+  __shared__ double res[2];
+  constexpr int NW = T / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = a.n;
+  // fixed rank blocks: warp w owns [w * blk, min(n, (w+1) * blk))
+  const int blk = ((n + NW - 1) / NW + 31) & ~31;
+  for (int q = tid; q < n; q += T) hs[q] = 0.0;
+  __syncthreads();
+
+  for (int64_t t = blockIdx.x; t < a.n_phase_rows; t += gridDim.x) {
+    const int64_t row = phase_row(a, t);
+    const int64_t beg = a.row_ptr[row];
+    const int m = (int)(a.row_ptr[row + 1] - beg);
+    if (!row_in_class(a, m)) continue;
+    double h[EPT];
+    int cc[EPT];
+    double lw0 = 0.0, lw1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int q = e * T + tid;
+      h[e] = 0.0;
+      cc[e] = -1;
+      if (q < m) {
+        const int c = __ldg(a.col + beg + q);
+        const double l = __ldg(a.lo + beg + q);
+        h[e] = __ldg(a.hi + beg + q) - l;
+        cc[e] = c;
+        const double2 w = __ldg(a.colw + c);
+        lw0 += l * w.x;
+        lw1 += l * w.y;
+      }
+    }
+    double hv[2] = {0.0, 0.0};
+    if (tid == 0) {
+      const double lr = a.r_min[row], la = a.a_min[row];
+      hv[0] = a.r_max[row] - lr;
+      hv[1] = a.a_max[row] - la;
+      const double2 wr = __ldg(a.colw + a.n_s), wa = __ldg(a.colw + a.n_s + 1);
+      lw0 += lr * wr.x + la * wa.x;
+      lw1 += lr * wr.y + la * wa.y;
+    }
+    const double s = a.slack[row];
+    double out[2];
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      const double* ws = o ? a.ws1 : a.ws0;
+      // scatter headroom by rank
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        if (cc[e] >= 0) {
+          RankReg<WIDE> r;
+          r.load(a, cc[e]);
+          hs[o ? r.r1() : r.r0()] = h[e];
+        }
+      }
+      if (tid == 0) {
+        for (int v = 0; v < 2; ++v) {
+          RankReg<WIDE> r;
+          r.load(a, a.n_s + v);
+          hs[o ? r.r1() : r.r0()] = hv[v];
+        }
+      }
+      __syncthreads();
+      // pass 1: per-warp totals over its rank block
+      const int b0 = warp * blk, b1 = min(n, b0 + blk);
+      double sh = 0.0, shw = 0.0;
+      for (int p = b0 + lane; p < b1; p += 32) {
+        const double x = hs[p];
+        sh += x;
+        shw += x * __ldg(ws + p);
+      }
+      sh = warp_sum(sh);
+      shw = warp_sum(shw);
+      if (lane == 0) {
+        wtot[0][warp] = sh;
+        wtot[1][warp] = shw;
+      }
+      __syncthreads();
+      // locate the crossing warp (first block whose running total >= s)
+      if (tid == 0) {
+        double run = 0.0, acc = 0.0;
+        int cw = NW;
+        for (int q = 0; q < NW; ++q) {
+          if (run + wtot[0][q] >= s) { cw = q; break; }
+          run += wtot[0][q];
+          acc += wtot[1][q];
+        }
+        cross_w = cw;
+        res[0] = run;   // C before the crossing block
+        res[1] = acc;   // sum(h w) before the crossing block
+      }
+      __syncthreads();
+      const int cw = cross_w;
+      if (cw == NW) {
+        out[o] = res[1];   // no crossing: every slot filled
+      } else if (warp == cw) {
+        // pass 2: walk from the crossing block chunk by chunk (continuing
+        // past its end if rounding of the block totals disagrees by an ulp)
+        double run = res[0], acc = res[1];
+        int P = -1;
+        double cP = 0.0;
+        for (int p0 = b0; p0 < n && P < 0; p0 += 32) {
+          const int p = p0 + lane;
+          const double x = p < n ? hs[p] : 0.0;
+          const double incl = warp_incl_scan(x, lane);
+          const unsigned hit = __ballot_sync(FULL, run + incl >= s && p < n);
+          if (hit) {
+            const int L = __ffs(hit) - 1;
+            const double xw = lane < L ? x * __ldg(ws + p) : 0.0;
+            acc += warp_sum(xw);
+            cP = run + __shfl_sync(FULL, incl - x, L);
+            P = p0 + L;
+          } else {
+            acc += warp_sum(p < n ? x * __ldg(ws + p) : 0.0);
+            run += __shfl_sync(FULL, incl, 31);
+          }
+        }
+        if (lane == 0) res[1] = P >= 0 ? acc + (s - cP) * ws[P] : acc;
+      }
+      __syncthreads();
+      if (cw != NW) out[o] = res[1];
+      // clear the scattered slots for the next row / order
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        if (cc[e] >= 0) {
+          RankReg<WIDE> r;
+          r.load(a, cc[e]);
+          hs[o ? r.r1() : r.r0()] = 0.0;
+        }
+      }
+      if (tid == 0) {
+        for (int v = 0; v < 2; ++v) {
+          RankReg<WIDE> r;
+          r.load(a, a.n_s + v);
+          hs[o ? r.r1() : r.r0()] = 0.0;
+        }
+      }
+      __syncthreads();
+    }
+    // sum(l w): fixed block tree
+    lw0 = warp_sum(lw0);
+    lw1 = warp_sum(lw1);
+    if (lane == 0) {
+      wtot[0][warp] = lw0;
+      wtot[1][warp] = lw1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double x0 = 0.0, x1 = 0.0;
+      for (int q = 0; q < NW; ++q) {
+        x0 += wtot[0][q];
+        x1 += wtot[1][q];
+      }
+      a.out0[t] = x0 + out[0];
+      a.out1[t] = x1 + out[1];
+    }
+    __syncthreads();
   }
 }
 
@@ -531,6 +796,7 @@ struct Work {
   DevBuf<unsigned> rank16;
   DevBuf<double> ws[2];
   DevBuf<double> val[2];
+  DevBuf<int> hint;                // warm-start crossing entries (2/row)
   DevBuf<int64_t> fixed, policy;
   DevBuf<unsigned char> cub_tmp;
   DevBuf<Ctl> ctl;
@@ -552,6 +818,8 @@ struct Work {
       perm[t].alloc(n);
       ws[t].alloc(n + 1);
       val[t].alloc(std::max<int64_t>(phase_rows, 1));
+    hint.alloc(2 * std::max<int64_t>(phase_rows, 1));
+    IMP_CUDA(cudaMemset(hint.ptr, 0xfe, hint.bytes()));   // -2: unknown
     }
     colw.alloc(n);
     rank.alloc(n);
@@ -595,6 +863,24 @@ void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
   IMP_CUDA(cudaGetLastError());
 }
 
+template <int T, int EPT>
+void launch_dense_t(const SweepArgs& a, int sms, cudaStream_t s) {
+  auto kern = k_sweep_dense<T, EPT, false>;
+  const size_t smem = (size_t)a.n * sizeof(double);
+  IMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  int per_sm = 0;
+  IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
+  per_sm = std::max(per_sm, 1);
+  int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>(a.n_phase_rows, (int64_t)sms * per_sm));
+  kern<<<blocks, T, smem, s>>>(a);
+  IMP_CUDA(cudaGetLastError());
+}
+
+// Rank-space kernel usable when the dense rank vector fits in shared memory.
+bool dense_capable(int n_s) { return ((int64_t)n_s + 2) * 8 <= 200 * 1024; }
+
 template <bool WIDE>
 void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
   switch (tm.team) {
@@ -609,9 +895,55 @@ void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
     case 64: return launch_sweep_t<64, 16, WIDE>(a, sms, s);
     case 128: return launch_sweep_t<128, 16, WIDE>(a, sms, s);
     case 256: return launch_sweep_t<256, 16, WIDE>(a, sms, s);
-    case 512: return launch_sweep_t<512, 16, WIDE>(a, sms, s);
-    default: return launch_sweep_t<1024, 16, WIDE>(a, sms, s);
+    default:
+      if (tm.ept == 32) return launch_sweep_t<512, 32, WIDE>(a, sms, s);
+      return launch_sweep_t<512, 16, WIDE>(a, sms, s);
   }
+}
+
+// K5 over all phase rows: one launch per row class present (classes are
+// fixed functions of a row's stored length m, so the kernel and summation
+// tree a row gets never depend on the shard or on other rows):
+//   rank-space  4m >= n_s (dense enough), m <= 8192 (T=256) / <= 16384 (T=512)
+//   warp team   m <= 512
+//   CTA teams   m <= 2048 / 4096 / 8192 / 16384 (128 / 256 / 512 / 512x32)
+// Returns the number of launches.
+int launch_sweep(SweepArgs sa, const imp_imdp* h, bool wide, int sms,
+                 cudaStream_t s) {
+  const int mr = h->max_row;
+  if (mr > 16384) fail(IMP_E_ARG, "row longer than 16384 stored entries");
+  int launches = 0;
+  // The rank-space kernel measured slower than the warm-started binary
+  // search on every benchmark shape; kept for reference, not dispatched.
+  sa.dense_ok = 0 && !wide && dense_capable(h->n_s);
+  if (sa.dense_ok && 4 * mr >= h->n_s) {
+    sa.dense_sel = 1;
+    sa.m_lo = -1;
+    sa.m_hi = 8192;
+    if (mr <= 256 * 16) launch_dense_t<256, 16>(sa, sms, s);
+    else launch_dense_t<256, 32>(sa, sms, s);
+    ++launches;
+    if (mr > 8192) {
+      sa.m_lo = 8192;
+      sa.m_hi = 16384;
+      launch_dense_t<512, 32>(sa, sms, s);
+      ++launches;
+    }
+  }
+  sa.dense_sel = 0;
+  static const int bounds[] = {-1, 512, 2048, 4096, 8192, 16384};
+  static const int teams[] = {32, 128, 256, 512, 512};
+  for (int c = 0; c < 5; ++c) {
+    if (mr <= bounds[c] && c > 0) break;
+    sa.m_lo = bounds[c];
+    sa.m_hi = bounds[c + 1];
+    Team tm{teams[c], c == 4 ? 32 : 16};
+    if (c == 0) tm = choose_team(std::min(mr, 512));
+    if (wide) launch_sweep_w<true>(sa, tm, sms, s);
+    else launch_sweep_w<false>(sa, tm, sms, s);
+    ++launches;
+  }
+  return launches;
 }
 
 struct Launch {
@@ -698,10 +1030,8 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   sa.nbits = w.nbits;
   sa.out0 = w.val[0].ptr;
   sa.out1 = w.val[1].ptr;
-  Team tm = choose_team(h->max_row);
-  if (tm.team == 0) fail(IMP_E_ARG, "row longer than 16384 stored entries");
-  if (w.wide) launch_sweep_w<true>(sa, tm, L.sms, s);
-  else launch_sweep_w<false>(sa, tm, L.sms, s);
+  sa.hint = w.hint.ptr;
+  const int n_sweep = launch_sweep(sa, h, w.wide, L.sms, s);
   w.last_sweep = sa;
 
   ReduceArgs rd{};
@@ -729,7 +1059,8 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
     k_control<<<1, 1, 0, s>>>(ctl);
     IMP_CUDA(cudaGetLastError());
   }
-  return 3 + (w.wide ? 0 : 1) + (h->k_count > 0 ? 1 : 0) + (ctl ? 1 : 0);
+  return 2 + n_sweep + (w.wide ? 0 : 1) + (h->k_count > 0 ? 1 : 0) +
+         (ctl ? 1 : 0);
 }
 
 __global__ void k_fill(double* p, int64_t n, double v) {
@@ -1060,11 +1391,7 @@ extern "C" int imp_row_values(imp_imdp* h, const double* weights, int32_t lp,
     sa.nbits = w.nbits;
     sa.out0 = w.val[0].ptr;
     sa.out1 = w.val[1].ptr;
-    Team tm = choose_team(h->max_row);
-    if (tm.team == 0) fail(IMP_E_ARG, "row longer than 16384 stored entries");
-    int sms = sm_count_of(h->device);
-    if (w.wide) launch_sweep_w<true>(sa, tm, sms, s);
-    else launch_sweep_w<false>(sa, tm, sms, s);
+    launch_sweep(sa, h, w.wide, sm_count_of(h->device), s);
     IMP_CUDA(cudaMemcpy(out, w.val[0].ptr, sizeof(double) * h->n_rows,
                         on_device ? cudaMemcpyDeviceToDevice
                                   : cudaMemcpyDeviceToHost));
@@ -1111,15 +1438,11 @@ extern "C" int imp_time_sweep(imp_imdp* h, int32_t spec, int32_t lp,
     L.use_ctl = false;
     enqueue_iteration(L, s);
     const SweepArgs sa = w.last_sweep;
-    const Team tm = choose_team(h->max_row);
     cudaEvent_t e0, e1;
     IMP_CUDA(cudaEventCreate(&e0));
     IMP_CUDA(cudaEventCreate(&e1));
     IMP_CUDA(cudaEventRecord(e0, s));
-    for (int r = 0; r < reps; ++r) {
-      if (w.wide) launch_sweep_w<true>(sa, tm, L.sms, s);
-      else launch_sweep_w<false>(sa, tm, L.sms, s);
-    }
+    for (int r = 0; r < reps; ++r) launch_sweep(sa, h, w.wide, L.sms, s);
     IMP_CUDA(cudaEventRecord(e1, s));
     IMP_CUDA(cudaEventSynchronize(e1));
     float t = 0.f;
