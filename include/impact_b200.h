@@ -144,6 +144,8 @@ typedef struct imp_build_stats {
   int64_t nnz;
   int64_t nm_instances;
   int64_t nm_evals;          /* objective evaluations (all NM instances)    */
+  int64_t nm_lane_slots;     /* refine-loop lane slots (warp trips x 32):
+                                nm_evals / nm_lane_slots = SIMT efficiency */
 } imp_build_stats;
 
 int imp_build(const imp_build_desc* desc, imp_imdp** out,

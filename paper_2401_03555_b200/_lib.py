@@ -56,7 +56,8 @@ class BuildStats(ctypes.Structure):
     _fields_ = [("ms_total", c_dbl), ("ms_mean_ranges", c_dbl),
                 ("ms_outer", c_dbl), ("ms_refine", c_dbl),
                 ("ms_assemble", c_dbl), ("nnz", c_i64),
-                ("nm_instances", c_i64), ("nm_evals", c_i64)]
+                ("nm_instances", c_i64), ("nm_evals", c_i64),
+                ("nm_lane_slots", c_i64)]
 
 
 class PhaseDesc(ctypes.Structure):

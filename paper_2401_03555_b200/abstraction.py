@@ -247,6 +247,7 @@ class BuildReport:
     nnz: int
     nm_instances: int
     nm_evals: int
+    nm_lane_slots: int    # refine-loop lane slots; evals / slots = SIMT eff.
     rows: int
     entries: int          # rows * n_s: the reference's `d`
 
@@ -273,7 +274,7 @@ def build_abstraction(dyn, noise, spaces, labels, opts=None,
     imdp.build_report = BuildReport(
         stats.ms_total, stats.ms_mean_ranges, stats.ms_outer,
         stats.ms_refine, stats.ms_assemble, stats.nnz, stats.nm_instances,
-        stats.nm_evals, rows, rows * desc.n_s)
+        stats.nm_evals, stats.nm_lane_slots, rows, rows * desc.n_s)
     return imdp
 
 

@@ -104,10 +104,14 @@ std::string config_header(const imp_build_desc* d) {
   o << "#define IMP_REFINE_BLOCK " << nm_block(d->n) << "\n";
   // tuning knobs (environment overrides for experiments)
   const char* minb = getenv("IMPACT_REFINE_MINB");
-  o << "#define IMP_REFINE_MINB " << (minb ? atoi(minb) : (d->n <= 4 ? 4 : 2))
+  o << "#define IMP_REFINE_MINB " << (minb ? atoi(minb) : (d->n <= 8 ? 4 : 2))
     << "\n";
   if (const char* ch = getenv("IMPACT_NDTR_CHUNK"))
     o << "#define IMP_NDTR_CHUNK " << atoi(ch) << "\n";
+  const char* vote = getenv("IMPACT_NDTR_VOTE");
+  o << "#define IMP_NDTR_VOTE " << (vote ? atoi(vote) : 0) << "\n";
+  const char* batch = getenv("IMPACT_REFINE_BATCH");
+  o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 2) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
   for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->n_deps[q];
   o << "};\n__device__ constexpr int kDeps[IMP_N][IMP_N] = {";
@@ -120,11 +124,13 @@ std::string config_header(const imp_build_desc* d) {
   return o.str();
 }
 
-std::string jit_source(const std::string& dyn_part) {
-  return std::string(kJitPrelude) + "\n" +
+// config header (macros, dependency tables) + ndtr prelude + generated
+// dynamics + kernels
+std::string jit_source(const std::string& config, const std::string& dyn) {
+  return config + std::string(kJitPrelude) + "\n" +
          "__device__ __forceinline__ double imp_min(double, double);\n"
          "__device__ __forceinline__ double imp_max(double, double);\n" +
-         dyn_part + "\n" + kJitKernels;
+         dyn + "\n" + kJitKernels;
 }
 
 // NVRTC: source -> sm_100a cubin (no device needed).
@@ -154,8 +160,8 @@ std::vector<char> compile_cubin(const std::string& src) {
   return cubin;
 }
 
-JitModule& jit(int device, const std::string& dyn_part) {
-  const std::string src = jit_source(dyn_part);
+JitModule& jit(int device, const std::string& config, const std::string& dyn) {
+  const std::string src = jit_source(config, dyn);
   const std::string key = std::to_string(device) + "\n" + src;
   std::lock_guard<std::mutex> lk(g_jit_mu);
   auto it = g_jit_cache.find(key);
@@ -237,7 +243,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     int sms = 148;
     IMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
                                     d->device));
-    JitModule& M = jit(d->device, config_header(d) + d->dyn_source);
+    JitModule& M = jit(d->device, config_header(d), d->dyn_source);
 
     cudaStream_t s;
     IMP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -309,10 +315,11 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     DevBuf<long long> aux_ptr(n_rows + 1);
     DevBuf<unsigned long long> err(3);
     DevBuf<double> err_val(3);
-    DevBuf<long long> evals(1);
+    // [0] objective evals, [1] refine lane slots, [2] refine work counter
+    DevBuf<long long> evals(3);
     IMP_CUDA(cudaMemsetAsync(err.ptr, 0xff, 3 * sizeof(unsigned long long), s));
     IMP_CUDA(cudaMemsetAsync(err_val.ptr, 0, 3 * sizeof(double), s));
-    IMP_CUDA(cudaMemsetAsync(evals.ptr, 0, sizeof(long long), s));
+    IMP_CUDA(cudaMemsetAsync(evals.ptr, 0, 3 * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(tcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(xcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(raw.ptr, 0, (n_rows * 6 + 1) * sizeof(double), s));
@@ -442,10 +449,12 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
 
     unsigned long long herr[3];
     double hval[3];
-    long long hev = 0;
+    long long hev = 0, hslots = 0;
     IMP_CUDA(cudaMemcpy(herr, err.ptr, sizeof(herr), cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(hval, err_val.ptr, sizeof(hval), cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(&hev, evals.ptr, sizeof(hev), cudaMemcpyDeviceToHost));
+    IMP_CUDA(cudaMemcpy(&hslots, evals.ptr + 1, sizeof(hslots),
+                        cudaMemcpyDeviceToHost));
     const long long row0 = (long long)d->k_begin * d->n_u * d->n_w;
     if (herr[0] != ~0ull) {
       set_error("row %lld", row0 + (long long)herr[0]);
@@ -476,6 +485,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
       stats->nnz = nnz;
       stats->nm_instances = instances;
       stats->nm_evals = hev;
+      stats->nm_lane_slots = hslots;
     }
     *out = h;
   });
@@ -489,7 +499,8 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
 extern "C" int imp_jit_compile(const imp_build_desc* d, const char* cubin_path) {
   return guarded([&] {
     IMP_REQUIRE(d && d->dyn_source, "null argument");
-    std::vector<char> cubin = compile_cubin(jit_source(config_header(d) + d->dyn_source));
+    std::vector<char> cubin =
+        compile_cubin(jit_source(config_header(d), d->dyn_source));
     if (cubin_path) {
       FILE* f = fopen(cubin_path, "wb");
       IMP_REQUIRE(f, "cannot open %s", cubin_path);

@@ -765,12 +765,14 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
   nm.max_evals = imp_max_evals(P, IMP_N);
   const int ms = imp_multistart(P, IMP_N);
   const long long total = 2 * P.n_items;
-  const long long nthreads = (long long)gridDim.x * blockDim.x;
-  const long long chunk = (total + nthreads - 1) / nthreads;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long g = tid * chunk;
-  const long long g_end = min(total, g + chunk);
-  if (g >= g_end) return;
+  // dynamic batches of consecutive instances from a global counter: a lane
+  // that finishes grabs the next batch, so warps stay full until the pool
+  // drains (NM instance costs vary 8..max_evals evaluations)
+  constexpr long long B = IMP_REFINE_BATCH;
+  unsigned long long* counter = (unsigned long long*)P.evals + 2;
+  long long g = (long long)atomicAdd(counter, (unsigned long long)B);
+  long long g_end = min(total, g + B);
+  if (g >= total) return;
   Instance I;
   imp_seek_instance(P, g, I);
 #pragma unroll
@@ -790,7 +792,9 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
   // is a nested branch that reconverges before the next evaluation, so a
   // warp never splits into groups evaluating the objective separately.
   bool live = true;
+  unsigned long long slots = 0;
   while (__any_sync(__activemask(), live)) {
+    ++slots;
     if (live) {
       double p[IMP_N];
       nm.point(p);
@@ -805,10 +809,18 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
         best = fmin(best, nm.best);
         if (++s == ms) {
           imp_store_instance(P, I, best);
-          if (++g >= g_end) {
+          bool more = ++g < g_end;
+          if (more) {
+            imp_next_instance(P, I);
+          } else {
+            g = (long long)atomicAdd(counter, (unsigned long long)B);
+            g_end = min(total, g + B);
+            more = g < total;
+            if (more) imp_seek_instance(P, g, I);
+          }
+          if (!more) {
             live = false;
           } else {
-            imp_next_instance(P, I);
 #pragma unroll
             for (int d = 0; d < IMP_N; ++d) {
               nm.lo[d] = I.clo[d];
@@ -828,6 +840,7 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
     __syncwarp(__activemask());
   }
   atomicAdd((unsigned long long*)P.evals, ev);
+  atomicAdd((unsigned long long*)P.evals + 1, slots);
 }
 
 
