@@ -21,6 +21,7 @@
 // row's contents and the shared order, never on its position or shard, so
 // bitwise-identical rows give bitwise-identical values.
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda_pipeline.h>
 
 #include <algorithm>
 #include <cmath>
@@ -246,11 +247,41 @@ __device__ __forceinline__ double2 team_sum2(double x, double y,
 // with one two-sided probe; otherwise the binary search runs.  Either way
 // the value is computed from C(<P*) with the same reduction, so the result
 // is independent of the hint (bitwise).
-template <int TEAM, int EPT, bool WIDE>
-__global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
+// First phase row >= t (stride nteams) whose length falls in this launch's
+// class, with its row / CSR start / length; team-uniform.
+__device__ __forceinline__ int64_t next_row(const SweepArgs& a, int64_t t,
+                                            int64_t nteams, int64_t& row,
+                                            int64_t& beg, int& m) {
+  for (; t < a.n_phase_rows; t += nteams) {
+    row = phase_row(a, t);
+    beg = a.row_ptr[row];
+    m = (int)(a.row_ptr[row + 1] - beg);
+    if (row_in_class(a, m)) return t;
+  }
+  return t;
+}
+
+// STAGED (CTA teams): the next row's col / lo / hi stream into a shared
+// memory stage with cp.async (LDGSTS) while the current row -- already in
+// registers -- is being priced, so HBM latency overlaps the reductions.
+template <int TEAM, int EPT, bool WIDE, bool STAGED = false>
+__global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
+                                  TEAM == 32 ? 2 : (TEAM < 512 ? 512 / TEAM : 1))
     k_sweep(SweepArgs a) {
   if (a.ctl && a.ctl->done) return;
   __shared__ double2 part[2 * (TEAM > 32 ? TEAM / 32 : 1)];
+  extern __shared__ double stage[];   // STAGED: lo[CAP] hi[CAP] col[CAP]
+  constexpr int CAP = TEAM * EPT;
+  // warp teams: one private stage per warp (20 B per entry = 2.5 doubles)
+  double* my_stage = TEAM == 32 ? stage + (threadIdx.x >> 5) * (CAP * 5 / 2)
+                                : stage;
+  double* s_lo = my_stage;
+  double* s_hi = my_stage + CAP;
+  int* s_col = reinterpret_cast<int*>(my_stage + 2 * CAP);
+  auto team_sync = [] {
+    if constexpr (TEAM == 32) __syncwarp();
+    else __syncthreads();
+  };
   int parity = 0;
   const int tid = TEAM == 32 ? (threadIdx.x & 31) : threadIdx.x;
   const int64_t team0 = TEAM == 32
@@ -259,30 +290,64 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
   const int64_t nteams = TEAM == 32
       ? (int64_t)gridDim.x * (blockDim.x >> 5) : (int64_t)gridDim.x;
 
-  for (int64_t t = team0; t < a.n_phase_rows; t += nteams) {
-    const int64_t row = phase_row(a, t);
-    const int64_t beg = a.row_ptr[row];
-    const int m = (int)(a.row_ptr[row + 1] - beg);
-    if (!row_in_class(a, m)) continue;
+  auto issue = [&](int64_t beg, int m) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const int q = e * TEAM + tid;
+      if (q < m) {
+        __pipeline_memcpy_async(s_lo + q, a.lo + beg + q, 8);
+        __pipeline_memcpy_async(s_hi + q, a.hi + beg + q, 8);
+        __pipeline_memcpy_async(s_col + q, a.col + beg + q, 4);
+      }
+    }
+    __pipeline_commit();
+  };
 
+  int64_t row = 0, beg = 0;
+  int m = 0;
+  int64_t t = next_row(a, team0, nteams, row, beg, m);
+  if constexpr (STAGED) {
+    if (t < a.n_phase_rows) issue(beg, m);
+  }
+  while (t < a.n_phase_rows) {
     double h[EPT];
     RankReg<WIDE> rk[EPT];
     double lw0 = 0.0, lw1 = 0.0;
+    int64_t row_n = 0, beg_n = 0;
+    int m_n = 0;
+    int64_t t_n;
+    if constexpr (STAGED) {
+      __pipeline_wait_prior(0);
+      team_sync();
+    }
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       h[e] = 0.0;
       rk[e].none();
       const int q = e * TEAM + tid;
       if (q < m) {
-        const int c = __ldg(a.col + beg + q);
-        const double l = __ldg(a.lo + beg + q);
-        const double u = __ldg(a.hi + beg + q);
+        int c;
+        double l, u;
+        if constexpr (STAGED) {
+          c = s_col[q];
+          l = s_lo[q];
+          u = s_hi[q];
+        } else {
+          c = __ldg(a.col + beg + q);
+          l = __ldg(a.lo + beg + q);
+          u = __ldg(a.hi + beg + q);
+        }
         h[e] = u - l;
         const double2 w = __ldg(a.colw + c);
         lw0 += l * w.x;
         lw1 += l * w.y;
         rk[e].load(a, c);
       }
+    }
+    if constexpr (STAGED) {
+      t_n = next_row(a, t + nteams, nteams, row_n, beg_n, m_n);
+      team_sync();                           // stage consumed
+      if (t_n < a.n_phase_rows) issue(beg_n, m_n);
     }
     // virtual slots n_s (target) and n_s + 1 (avoid) on team thread 0
     double hv[2] = {0.0, 0.0};
@@ -403,6 +468,11 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM)
       a.out0[t] = lw.x + x0;
       a.out1[t] = lw.y + x1;
     }
+    if constexpr (!STAGED) t_n = next_row(a, t + nteams, nteams, row_n, beg_n, m_n);
+    t = t_n;
+    row = row_n;
+    beg = beg_n;
+    m = m_n;
   }
 }
 
@@ -850,16 +920,26 @@ Team choose_team(int max_row) {
 
 template <int TEAM, int EPT, bool WIDE>
 void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
-  auto kern = k_sweep<TEAM, EPT, WIDE>;
+  // CTA teams stage the next row through shared memory when one row of
+  // col/lo/hi (20 B per entry) fits
+  // (warp teams: one stage per warp, 8 warps per block)
+  constexpr int PER_BLOCK = TEAM == 32 ? 8 : 1;
+  constexpr bool STAGED = TEAM * EPT * 20 * PER_BLOCK <= 200 * 1024 &&
+                          (TEAM > 32 || EPT >= 4);
+  auto kern = k_sweep<TEAM, EPT, WIDE, STAGED>;
+  const size_t smem = STAGED ? (size_t)TEAM * EPT * 20 * PER_BLOCK : 0;
+  if (smem > 48 * 1024)
+    IMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
   int threads = TEAM == 32 ? 256 : TEAM;
   int per_sm = 0;
   IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
-                                                         threads, 0));
+                                                         threads, smem));
   per_sm = std::max(per_sm, 1);
   int64_t teams_per_block = TEAM == 32 ? threads / 32 : 1;
   int64_t need = (a.n_phase_rows + teams_per_block - 1) / teams_per_block;
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * per_sm));
-  kern<<<blocks, threads, 0, s>>>(a);
+  kern<<<blocks, threads, smem, s>>>(a);
   IMP_CUDA(cudaGetLastError());
 }
 
