@@ -104,10 +104,11 @@ std::string config_header(const imp_build_desc* d) {
   o << "#define IMP_REFINE_BLOCK " << nm_block(d->n) << "\n";
   // tuning knobs (environment overrides for experiments)
   const char* minb = getenv("IMPACT_REFINE_MINB");
+  // defaults measured on the full vehicle3d / room5d builds (subsets mislead)
   o << "#define IMP_REFINE_MINB " << (minb ? atoi(minb) : (d->n <= 8 ? 4 : 2))
     << "\n";
-  if (const char* ch = getenv("IMPACT_NDTR_CHUNK"))
-    o << "#define IMP_NDTR_CHUNK " << atoi(ch) << "\n";
+  const char* ch = getenv("IMPACT_NDTR_CHUNK");
+  o << "#define IMP_NDTR_CHUNK " << (ch ? atoi(ch) : 1) << "\n";
   const char* vote = getenv("IMPACT_NDTR_VOTE");
   o << "#define IMP_NDTR_VOTE " << (vote ? atoi(vote) : 0) << "\n";
   const char* batch = getenv("IMPACT_REFINE_BATCH");
