@@ -167,12 +167,11 @@ struct SweepArgs {
   const int64_t* fixed;     // phase-2 policy (local states) or nullptr
   int64_t n_phase_rows;
   int n_u, n_w, n_s, n, nbits;
-  // row class handled by this launch (fixed thresholds on the row's own
+  // phase rows of this launch's class (a fixed function of the row's own
   // stored length m, so the kernel -- hence the summation tree -- a row
   // gets never depends on its shard or neighbours)
-  int m_lo, m_hi;       // m_lo < m <= m_hi
-  int dense_sel;        // 1: rows of the rank-space class, 0: the others
-  int dense_ok;         // rank-space kernel usable for this n
+  const int* list;
+  int64_t n_list;
   int* hint;            // (2 * n_phase_rows) warm-start crossing entries
   double* out0;
   double* out1;
@@ -202,11 +201,6 @@ struct RankReg<true> {
   }
   __device__ __forceinline__ void none() { x = y = 0x7fffffff; }
 };
-
-__device__ __forceinline__ bool row_in_class(const SweepArgs& a, int m) {
-  const bool dense = a.dense_ok && 4 * m >= a.n_s;
-  return dense == (a.dense_sel != 0) && m > a.m_lo && m <= a.m_hi;
-}
 
 __device__ __forceinline__ int64_t phase_row(const SweepArgs& a, int64_t t) {
   if (!a.fixed) return t;
@@ -247,18 +241,15 @@ __device__ __forceinline__ double2 team_sum2(double x, double y,
 // with one two-sided probe; otherwise the binary search runs.  Either way
 // the value is computed from C(<P*) with the same reduction, so the result
 // is independent of the hint (bitwise).
-// First phase row >= t (stride nteams) whose length falls in this launch's
-// class, with its row / CSR start / length; team-uniform.
-__device__ __forceinline__ int64_t next_row(const SweepArgs& a, int64_t t,
-                                            int64_t nteams, int64_t& row,
-                                            int64_t& beg, int& m) {
-  for (; t < a.n_phase_rows; t += nteams) {
-    row = phase_row(a, t);
-    beg = a.row_ptr[row];
-    m = (int)(a.row_ptr[row + 1] - beg);
-    if (row_in_class(a, m)) return t;
-  }
-  return t;
+// i-th row of this launch's class list: phase row t, CSR row, start,
+// length; team-uniform.
+__device__ __forceinline__ void class_row(const SweepArgs& a, int64_t i,
+                                         int64_t& t, int64_t& row,
+                                         int64_t& beg, int& m) {
+  t = a.list[i];
+  row = phase_row(a, t);
+  beg = a.row_ptr[row];
+  m = (int)(a.row_ptr[row + 1] - beg);
 }
 
 // STAGED (CTA teams): the next row's col / lo / hi stream into a shared
@@ -303,19 +294,20 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     __pipeline_commit();
   };
 
-  int64_t row = 0, beg = 0;
+  int64_t row = 0, beg = 0, t = 0;
   int m = 0;
-  int64_t t = next_row(a, team0, nteams, row, beg, m);
+  int64_t i = team0;
+  if (i < a.n_list) class_row(a, i, t, row, beg, m);
   if constexpr (STAGED) {
-    if (t < a.n_phase_rows) issue(beg, m);
+    if (i < a.n_list) issue(beg, m);
   }
-  while (t < a.n_phase_rows) {
+  while (i < a.n_list) {
     double h[EPT];
     RankReg<WIDE> rk[EPT];
     double lw0 = 0.0, lw1 = 0.0;
-    int64_t row_n = 0, beg_n = 0;
+    int64_t row_n = 0, beg_n = 0, t_n = 0;
     int m_n = 0;
-    int64_t t_n;
+    const int64_t i_n = i + nteams;
     if constexpr (STAGED) {
       __pipeline_wait_prior(0);
       team_sync();
@@ -345,9 +337,9 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
       }
     }
     if constexpr (STAGED) {
-      t_n = next_row(a, t + nteams, nteams, row_n, beg_n, m_n);
+      if (i_n < a.n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
       team_sync();                           // stage consumed
-      if (t_n < a.n_phase_rows) issue(beg_n, m_n);
+      if (i_n < a.n_list) issue(beg_n, m_n);
     }
     // virtual slots n_s (target) and n_s + 1 (avoid) on team thread 0
     double hv[2] = {0.0, 0.0};
@@ -468,7 +460,10 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
       a.out0[t] = lw.x + x0;
       a.out1[t] = lw.y + x1;
     }
-    if constexpr (!STAGED) t_n = next_row(a, t + nteams, nteams, row_n, beg_n, m_n);
+    if constexpr (!STAGED) {
+      if (i_n < a.n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
+    }
+    i = i_n;
     t = t_n;
     row = row_n;
     beg = beg_n;
@@ -476,198 +471,6 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
   }
 }
 
-
-// ---------------------------------------------------------------------------
-// K5 variant for wide rows (live entries a large fraction of the columns:
-// vehicle3d, dim14).  Rank-space form of the same greedy fill: a CTA
-// scatters the row's headroom into a dense shared-memory vector indexed by
-// global rank, then scans it in rank order -- O(n) shared-memory work per
-// row instead of log2(n) team reductions, no binary search.
-//   pass 1  every warp totals sum(h) and sum(h * w_sorted) over a fixed
-//           contiguous block of ranks (coalesced chunks of 32);
-//   scan    block exclusive scan of the warp totals (fixed tree) locates
-//           the warp whose block holds the crossing;
-//   pass 2  that warp walks its block chunk by chunk (warp inclusive scan)
-//           to the crossing rank P and its partial sums;
-// value = sum(l*w) + sum_{rank<P} h w + (slack - C(<P)) w_sorted[P].
-// The partition of ranks into warps / chunks / lanes depends only on n, so
-// results depend only on the row's contents (position independent).
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    double t = __shfl_up_sync(FULL, v, o);
-    if (lane >= o) v += t;
-  }
-  return v;
-}
-
-template <int T, int EPT, bool WIDE>
-__global__ void __launch_bounds__(T) k_sweep_dense(SweepArgs a) {
-  if (a.ctl && a.ctl->done) return;
-  extern __shared__ double hs[];            // (n) headroom by rank
-  __shared__ double wtot[2][T / 32];        // per-warp sum(h), sum(h w)
-  __shared__ int cross_w;
-  __shared__ double res[2];
-  constexpr int NW = T / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = a.n;
-  // fixed rank blocks: warp w owns [w * blk, min(n, (w+1) * blk))
-  const int blk = ((n + NW - 1) / NW + 31) & ~31;
-  for (int q = tid; q < n; q += T) hs[q] = 0.0;
-  __syncthreads();
-
-  for (int64_t t = blockIdx.x; t < a.n_phase_rows; t += gridDim.x) {
-    const int64_t row = phase_row(a, t);
-    const int64_t beg = a.row_ptr[row];
-    const int m = (int)(a.row_ptr[row + 1] - beg);
-    if (!row_in_class(a, m)) continue;
-    double h[EPT];
-    int cc[EPT];
-    double lw0 = 0.0, lw1 = 0.0;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int q = e * T + tid;
-      h[e] = 0.0;
-      cc[e] = -1;
-      if (q < m) {
-        const int c = __ldg(a.col + beg + q);
-        const double l = __ldg(a.lo + beg + q);
-        h[e] = __ldg(a.hi + beg + q) - l;
-        cc[e] = c;
-        const double2 w = __ldg(a.colw + c);
-        lw0 += l * w.x;
-        lw1 += l * w.y;
-      }
-    }
-    double hv[2] = {0.0, 0.0};
-    if (tid == 0) {
-      const double lr = a.r_min[row], la = a.a_min[row];
-      hv[0] = a.r_max[row] - lr;
-      hv[1] = a.a_max[row] - la;
-      const double2 wr = __ldg(a.colw + a.n_s), wa = __ldg(a.colw + a.n_s + 1);
-      lw0 += lr * wr.x + la * wa.x;
-      lw1 += lr * wr.y + la * wa.y;
-    }
-    const double s = a.slack[row];
-    double out[2];
-#pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      const double* ws = o ? a.ws1 : a.ws0;
-      // scatter headroom by rank
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        if (cc[e] >= 0) {
-          RankReg<WIDE> r;
-          r.load(a, cc[e]);
-          hs[o ? r.r1() : r.r0()] = h[e];
-        }
-      }
-      if (tid == 0) {
-        for (int v = 0; v < 2; ++v) {
-          RankReg<WIDE> r;
-          r.load(a, a.n_s + v);
-          hs[o ? r.r1() : r.r0()] = hv[v];
-        }
-      }
-      __syncthreads();
-      // pass 1: per-warp totals over its rank block
-      const int b0 = warp * blk, b1 = min(n, b0 + blk);
-      double sh = 0.0, shw = 0.0;
-      for (int p = b0 + lane; p < b1; p += 32) {
-        const double x = hs[p];
-        sh += x;
-        shw += x * __ldg(ws + p);
-      }
-      sh = warp_sum(sh);
-      shw = warp_sum(shw);
-      if (lane == 0) {
-        wtot[0][warp] = sh;
-        wtot[1][warp] = shw;
-      }
-      __syncthreads();
-      // locate the crossing warp (first block whose running total >= s)
-      if (tid == 0) {
-        double run = 0.0, acc = 0.0;
-        int cw = NW;
-        for (int q = 0; q < NW; ++q) {
-          if (run + wtot[0][q] >= s) { cw = q; break; }
-          run += wtot[0][q];
-          acc += wtot[1][q];
-        }
-        cross_w = cw;
-        res[0] = run;   // C before the crossing block
-        res[1] = acc;   // sum(h w) before the crossing block
-      }
-      __syncthreads();
-      const int cw = cross_w;
-      if (cw == NW) {
-        out[o] = res[1];   // no crossing: every slot filled
-      } else if (warp == cw) {
-        // pass 2: walk from the crossing block chunk by chunk (continuing
-        // past its end if rounding of the block totals disagrees by an ulp)
-        double run = res[0], acc = res[1];
-        int P = -1;
-        double cP = 0.0;
-        for (int p0 = b0; p0 < n && P < 0; p0 += 32) {
-          const int p = p0 + lane;
-          const double x = p < n ? hs[p] : 0.0;
-          const double incl = warp_incl_scan(x, lane);
-          const unsigned hit = __ballot_sync(FULL, run + incl >= s && p < n);
-          if (hit) {
-            const int L = __ffs(hit) - 1;
-            const double xw = lane < L ? x * __ldg(ws + p) : 0.0;
-            acc += warp_sum(xw);
-            cP = run + __shfl_sync(FULL, incl - x, L);
-            P = p0 + L;
-          } else {
-            acc += warp_sum(p < n ? x * __ldg(ws + p) : 0.0);
-            run += __shfl_sync(FULL, incl, 31);
-          }
-        }
-        if (lane == 0) res[1] = P >= 0 ? acc + (s - cP) * ws[P] : acc;
-      }
-      __syncthreads();
-      if (cw != NW) out[o] = res[1];
-      // clear the scattered slots for the next row / order
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        if (cc[e] >= 0) {
-          RankReg<WIDE> r;
-          r.load(a, cc[e]);
-          hs[o ? r.r1() : r.r0()] = 0.0;
-        }
-      }
-      if (tid == 0) {
-        for (int v = 0; v < 2; ++v) {
-          RankReg<WIDE> r;
-          r.load(a, a.n_s + v);
-          hs[o ? r.r1() : r.r0()] = 0.0;
-        }
-      }
-      __syncthreads();
-    }
-    // sum(l w): fixed block tree
-    lw0 = warp_sum(lw0);
-    lw1 = warp_sum(lw1);
-    if (lane == 0) {
-      wtot[0][warp] = lw0;
-      wtot[1][warp] = lw1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double x0 = 0.0, x1 = 0.0;
-      for (int q = 0; q < NW; ++q) {
-        x0 += wtot[0][q];
-        x1 += wtot[1][q];
-      }
-      a.out0[t] = x0 + out[0];
-      a.out1[t] = x1 + out[1];
-    }
-    __syncthreads();
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Robust Bellman reduction + convergence statistics
@@ -872,6 +675,12 @@ struct Work {
   DevBuf<Ctl> ctl;
   size_t cub_bytes = 0;
   SweepArgs last_sweep{};   // arguments of the last enqueued K5 launch
+  // K5 row classes: phase rows grouped by class (see launch_sweep)
+  static constexpr int NCLASS = 8;
+  DevBuf<int> class_rows;
+  DevBuf<unsigned long long> class_cnt;   // counts, then scatter cursors
+  int64_t class_off[NCLASS + 1] = {};
+  bool classes_all = false;   // class lists hold the unfixed phase
 
   void init(const imp_imdp* h, int64_t phase_rows) {
     n_s = h->n_s;
@@ -888,9 +697,11 @@ struct Work {
       perm[t].alloc(n);
       ws[t].alloc(n + 1);
       val[t].alloc(std::max<int64_t>(phase_rows, 1));
+    }
     hint.alloc(2 * std::max<int64_t>(phase_rows, 1));
     IMP_CUDA(cudaMemset(hint.ptr, 0xfe, hint.bytes()));   // -2: unknown
-    }
+    class_rows.alloc(std::max<int64_t>(phase_rows, 1));
+    class_cnt.alloc(2 * NCLASS);
     colw.alloc(n);
     rank.alloc(n);
     if (!wide) rank16.alloc(n);
@@ -904,6 +715,84 @@ struct Work {
     ctl.alloc(1);
   }
 };
+
+// Row classes of K5 by stored length (upper bounds, inclusive); a pure
+// function of the row, so the kernel a row gets never depends on its shard.
+__constant__ int kClassHi[8] = {128, 256, 384, 512, 2048, 4096, 8192, 16384};
+
+__device__ __forceinline__ int row_class(int m) {
+  int c = 0;
+  while (c < 7 && m > kClassHi[c]) ++c;
+  return c;
+}
+
+__device__ __forceinline__ int64_t phase_row_of(const int64_t* fixed, int n_u,
+                                                int n_w, int64_t t) {
+  if (!fixed) return t;
+  int64_t k = t / n_w, i = t - k * n_w;
+  return (k * n_u + fixed[k]) * n_w + i;
+}
+
+__global__ void k_class_count(const int64_t* row_ptr, const int64_t* fixed,
+                              int n_u, int n_w, int64_t rows,
+                              unsigned long long* cnt) {
+  __shared__ unsigned int local[8];
+  if (threadIdx.x < 8) local[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = phase_row_of(fixed, n_u, n_w, t);
+    atomicAdd(&local[row_class((int)(row_ptr[r + 1] - row_ptr[r]))], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 && local[threadIdx.x])
+    atomicAdd(cnt + threadIdx.x, (unsigned long long)local[threadIdx.x]);
+}
+
+// order within a class is irrelevant: rows are independent and outputs are
+// indexed by phase row
+__global__ void k_class_scatter(const int64_t* row_ptr, const int64_t* fixed,
+                                int n_u, int n_w, int64_t rows,
+                                unsigned long long* cursor, int* out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = phase_row_of(fixed, n_u, n_w, t);
+    const int c = row_class((int)(row_ptr[r + 1] - row_ptr[r]));
+    out[atomicAdd(cursor + c, 1ull)] = (int)t;
+  }
+}
+
+void build_classes(const imp_imdp* h, Work& w, const int64_t* fixed_dev,
+                   int64_t phase_rows, cudaStream_t s) {
+  if (h->max_row > 16384) fail(IMP_E_ARG, "row longer than 16384 stored entries");
+  IMP_CUDA(cudaMemsetAsync(w.class_cnt.ptr, 0, w.class_cnt.bytes(), s));
+  const int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((phase_rows + 255) / 256, 148 * 8));
+  if (phase_rows > 0) {
+    k_class_count<<<blocks, 256, 0, s>>>(h->row_ptr.ptr, fixed_dev, h->n_u,
+                                         h->n_w, phase_rows, w.class_cnt.ptr);
+    IMP_CUDA(cudaGetLastError());
+  }
+  unsigned long long cnt[Work::NCLASS];
+  IMP_CUDA(cudaMemcpyAsync(cnt, w.class_cnt.ptr, sizeof(cnt),
+                           cudaMemcpyDeviceToHost, s));
+  IMP_CUDA(cudaStreamSynchronize(s));
+  w.class_off[0] = 0;
+  for (int c = 0; c < Work::NCLASS; ++c) w.class_off[c + 1] = w.class_off[c] + cnt[c];
+  unsigned long long cur[Work::NCLASS];
+  for (int c = 0; c < Work::NCLASS; ++c) cur[c] = w.class_off[c];
+  IMP_CUDA(cudaMemcpyAsync(w.class_cnt.ptr + Work::NCLASS, cur, sizeof(cur),
+                           cudaMemcpyHostToDevice, s));
+  if (phase_rows > 0) {
+    k_class_scatter<<<blocks, 256, 0, s>>>(h->row_ptr.ptr, fixed_dev, h->n_u,
+                                           h->n_w, phase_rows,
+                                           w.class_cnt.ptr + Work::NCLASS,
+                                           w.class_rows.ptr);
+    IMP_CUDA(cudaGetLastError());
+  }
+  IMP_CUDA(cudaStreamSynchronize(s));
+  count_launches(phase_rows > 0 ? 2 : 0, 0);
+}
 
 struct Team {
   int team, ept;
@@ -937,29 +826,12 @@ void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
                                                          threads, smem));
   per_sm = std::max(per_sm, 1);
   int64_t teams_per_block = TEAM == 32 ? threads / 32 : 1;
-  int64_t need = (a.n_phase_rows + teams_per_block - 1) / teams_per_block;
+  int64_t need = (a.n_list + teams_per_block - 1) / teams_per_block;
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * per_sm));
   kern<<<blocks, threads, smem, s>>>(a);
   IMP_CUDA(cudaGetLastError());
 }
 
-template <int T, int EPT>
-void launch_dense_t(const SweepArgs& a, int sms, cudaStream_t s) {
-  auto kern = k_sweep_dense<T, EPT, false>;
-  const size_t smem = (size_t)a.n * sizeof(double);
-  IMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-  int per_sm = 0;
-  IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
-  per_sm = std::max(per_sm, 1);
-  int blocks = (int)std::max<int64_t>(
-      1, std::min<int64_t>(a.n_phase_rows, (int64_t)sms * per_sm));
-  kern<<<blocks, T, smem, s>>>(a);
-  IMP_CUDA(cudaGetLastError());
-}
-
-// Rank-space kernel usable when the dense rank vector fits in shared memory.
-bool dense_capable(int n_s) { return ((int64_t)n_s + 2) * 8 <= 200 * 1024; }
 
 template <bool WIDE>
 void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
@@ -970,6 +842,7 @@ void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
         case 2: return launch_sweep_t<32, 2, WIDE>(a, sms, s);
         case 4: return launch_sweep_t<32, 4, WIDE>(a, sms, s);
         case 8: return launch_sweep_t<32, 8, WIDE>(a, sms, s);
+        case 12: return launch_sweep_t<32, 12, WIDE>(a, sms, s);
         default: return launch_sweep_t<32, 16, WIDE>(a, sms, s);
       }
     case 64: return launch_sweep_t<64, 16, WIDE>(a, sms, s);
@@ -981,44 +854,24 @@ void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
   }
 }
 
-// K5 over all phase rows: one launch per row class present (classes are
-// fixed functions of a row's stored length m, so the kernel and summation
-// tree a row gets never depend on the shard or on other rows):
-//   rank-space  4m >= n_s (dense enough), m <= 8192 (T=256) / <= 16384 (T=512)
-//   warp team   m <= 512
+// K5 over all phase rows: one launch per non-empty row class (classes are
+// fixed functions of a row's stored length m -- see kClassHi -- so the
+// kernel and summation tree a row gets never depend on the shard):
+//   warp team   m <= 128 / 256 / 384 / 512 (EPT 4 / 8 / 12 / 16; padding
+//               adds +0.0 and does not change any sum)
 //   CTA teams   m <= 2048 / 4096 / 8192 / 16384 (128 / 256 / 512 / 512x32)
 // Returns the number of launches.
-int launch_sweep(SweepArgs sa, const imp_imdp* h, bool wide, int sms,
+int launch_sweep(SweepArgs sa, const Work& w, bool wide, int sms,
                  cudaStream_t s) {
-  const int mr = h->max_row;
-  if (mr > 16384) fail(IMP_E_ARG, "row longer than 16384 stored entries");
+  static const int teams[] = {32, 32, 32, 32, 128, 256, 512, 512};
+  static const int epts[] = {4, 8, 12, 16, 16, 16, 16, 32};
   int launches = 0;
-  // The rank-space kernel measured slower than the warm-started binary
-  // search on every benchmark shape; kept for reference, not dispatched.
-  sa.dense_ok = 0 && !wide && dense_capable(h->n_s);
-  if (sa.dense_ok && 4 * mr >= h->n_s) {
-    sa.dense_sel = 1;
-    sa.m_lo = -1;
-    sa.m_hi = 8192;
-    if (mr <= 256 * 16) launch_dense_t<256, 16>(sa, sms, s);
-    else launch_dense_t<256, 32>(sa, sms, s);
-    ++launches;
-    if (mr > 8192) {
-      sa.m_lo = 8192;
-      sa.m_hi = 16384;
-      launch_dense_t<512, 32>(sa, sms, s);
-      ++launches;
-    }
-  }
-  sa.dense_sel = 0;
-  static const int bounds[] = {-1, 512, 2048, 4096, 8192, 16384};
-  static const int teams[] = {32, 128, 256, 512, 512};
-  for (int c = 0; c < 5; ++c) {
-    if (mr <= bounds[c] && c > 0) break;
-    sa.m_lo = bounds[c];
-    sa.m_hi = bounds[c + 1];
-    Team tm{teams[c], c == 4 ? 32 : 16};
-    if (c == 0) tm = choose_team(std::min(mr, 512));
+  for (int c = 0; c < Work::NCLASS; ++c) {
+    const int64_t cnt = w.class_off[c + 1] - w.class_off[c];
+    if (cnt == 0) continue;
+    sa.list = w.class_rows.ptr + w.class_off[c];
+    sa.n_list = cnt;
+    Team tm{teams[c], epts[c]};
     if (wide) launch_sweep_w<true>(sa, tm, sms, s);
     else launch_sweep_w<false>(sa, tm, sms, s);
     ++launches;
@@ -1111,7 +964,7 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   sa.out0 = w.val[0].ptr;
   sa.out1 = w.val[1].ptr;
   sa.hint = w.hint.ptr;
-  const int n_sweep = launch_sweep(sa, h, w.wide, L.sms, s);
+  const int n_sweep = launch_sweep(sa, w, w.wide, L.sms, s);
   w.last_sweep = sa;
 
   ReduceArgs rd{};
@@ -1185,6 +1038,7 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
                                sizeof(int64_t) * h->k_count,
                                cudaMemcpyHostToDevice, s));
     }
+    build_classes(h, w, d->fixed_policy ? w.fixed.ptr : nullptr, phase_rows, s);
     for (int p = 0; p < 2; ++p) {
       fill(w.v[0][p].ptr, h->n_s, 0.0, s);
       fill(w.v[1][p].ptr, h->n_s, 1.0, s);
@@ -1318,6 +1172,12 @@ void explicit_step(imp_imdp* h, const double* v0, const double* v1, int spec,
   const int64_t phase_rows = fixed_dev ? (int64_t)h->k_count * h->n_w
                                        : h->n_rows;
   Work& w = cached_work(h, phase_rows);
+  // classes of the unfixed phase are a property of the handle; a fixed
+  // policy's may change between calls
+  if (fixed_dev || !w.classes_all) {
+    build_classes(h, w, fixed_dev, phase_rows, s);
+    w.classes_all = !fixed_dev;
+  }
   Launch L{};
   L.h = h;
   L.w = &w;
@@ -1471,7 +1331,8 @@ extern "C" int imp_row_values(imp_imdp* h, const double* weights, int32_t lp,
     sa.nbits = w.nbits;
     sa.out0 = w.val[0].ptr;
     sa.out1 = w.val[1].ptr;
-    launch_sweep(sa, h, w.wide, sm_count_of(h->device), s);
+    build_classes(h, w, nullptr, h->n_rows, s);
+    launch_sweep(sa, w, w.wide, sm_count_of(h->device), s);
     IMP_CUDA(cudaMemcpy(out, w.val[0].ptr, sizeof(double) * h->n_rows,
                         on_device ? cudaMemcpyDeviceToDevice
                                   : cudaMemcpyDeviceToHost));
@@ -1516,13 +1377,14 @@ extern "C" int imp_time_sweep(imp_imdp* h, int32_t spec, int32_t lp,
     L.new_explicit[1] = n1.ptr;
     L.stats_explicit = st.ptr;
     L.use_ctl = false;
+    build_classes(h, w, nullptr, h->n_rows, s);
     enqueue_iteration(L, s);
     const SweepArgs sa = w.last_sweep;
     cudaEvent_t e0, e1;
     IMP_CUDA(cudaEventCreate(&e0));
     IMP_CUDA(cudaEventCreate(&e1));
     IMP_CUDA(cudaEventRecord(e0, s));
-    for (int r = 0; r < reps; ++r) launch_sweep(sa, h, w.wide, L.sms, s);
+    for (int r = 0; r < reps; ++r) launch_sweep(sa, w, w.wide, L.sms, s);
     IMP_CUDA(cudaEventRecord(e1, s));
     IMP_CUDA(cudaEventSynchronize(e1));
     float t = 0.f;
