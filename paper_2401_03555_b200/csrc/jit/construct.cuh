@@ -33,8 +33,11 @@ __device__ __forceinline__ double imp_min(double a, double b) {
 __device__ __forceinline__ double imp_max(double a, double b) {
   return (a > b || a != a) ? a : b;
 }
+// np.clip on non-NaN values, signed zeros included: numpy's clip loop is
+// min(max(x, lo), hi) with max(a, b) = a > b ? a : b, min(a, b) = a < b ? a : b
 __device__ __forceinline__ double imp_clip(double x, double lo, double hi) {
-  return fmin(fmax(x, lo), hi);       // np.clip on finite values
+  const double t = x > lo ? x : lo;
+  return t < hi ? t : hi;
 }
 __device__ __forceinline__ bool imp_finite(double x) {
   return x - x == 0.0;
@@ -716,8 +719,8 @@ __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
   for (int d = 0; d < IMP_N; ++d) {
     const double m = mean[d];
     const double s = P.sigma[d];
-    arg[2 * d] = (I.bhi[d] - m) / s;
-    arg[2 * d + 1] = (I.blo[d] - m) / s;
+    arg[2 * d] = imp_div(I.bhi[d] - m, s);
+    arg[2 * d + 1] = imp_div(I.blo[d] - m, s);
   }
 #ifndef IMP_NDTR_CHUNK
 #define IMP_NDTR_CHUNK 1

@@ -401,6 +401,8 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
             a, b = emit(node[2]), emit(node[3])
             if node[1] == "^":
                 return f"pow({a}, {b})"
+            if node[1] == "/":
+                return f"imp_div({a}, {b})"
             return f"({a} {node[1]} {b})"
         if tag == "call":
             return f"{_CUDA_FN[node[1]]}({', '.join(emit(a) for a in node[2])})"
@@ -486,7 +488,12 @@ def _emit_all(dyn, fold, xfree):
             s = f"(-{gen(node[1])})"
         elif tag == "bin":
             a, b = gen(node[2]), gen(node[3])
-            s = f"pow({a}, {b})" if node[1] == "^" else f"({a} {node[1]} {b})"
+            if node[1] == "^":
+                s = f"pow({a}, {b})"
+            elif node[1] == "/":   # ndtr.h: IEEE divide without the 0/d slow path
+                s = f"imp_div({a}, {b})"
+            else:
+                s = f"({a} {node[1]} {b})"
         else:
             s = f"{_CUDA_FN[node[1]]}({', '.join(gen(a) for a in node[2])})"
         if seen[node] > 1 or tag == "call":

@@ -7,9 +7,10 @@ import bench
 
 name = sys.argv[1]
 synth = len(sys.argv) > 2 and sys.argv[2] == "synth"
+reps = 1 if len(sys.argv) > 2 and sys.argv[2] == "once" else 2
 cfg = benchmark(name)
 labels = cfg.labels()
-for rep in range(2):
+for rep in range(reps):
     t0 = time.perf_counter()
     im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels, cfg.abstraction_options())
     t1 = time.perf_counter()
