@@ -73,6 +73,8 @@ struct BuildParams {
   double* a_max;
   unsigned long long* err;
   double* err_val;
+  double sig[16];
+  double sig_rcp[16];
 };
 
 // JIT modules go through the runtime's library API (cudaLibrary_t /
@@ -109,8 +111,6 @@ std::string config_header(const imp_build_desc* d) {
     << "\n";
   const char* ch = getenv("IMPACT_NDTR_CHUNK");
   o << "#define IMP_NDTR_CHUNK " << (ch ? atoi(ch) : 1) << "\n";
-  const char* vote = getenv("IMPACT_NDTR_VOTE");
-  o << "#define IMP_NDTR_VOTE " << (vote ? atoi(vote) : 0) << "\n";
   const char* batch = getenv("IMPACT_REFINE_BATCH");
   o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 2) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
@@ -340,6 +340,11 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     P.strides = g_strides.ptr;
     P.eta = g_eta.ptr;
     P.sigma = g_sigma.ptr;
+    for (int q = 0; q < 16; ++q) {
+      const double sg = q < N ? d->sigma[q] : 1.0;
+      P.sig[q] = sg;
+      P.sig_rcp[q] = (sg >= 0x1p-100 && sg <= 0x1p100) ? 1.0 / sg : NAN;
+    }
     P.edges = g_edges.ptr;
     P.cover_lo = g_clo.ptr;
     P.cover_hi = g_chi.ptr;

@@ -96,6 +96,10 @@ struct BuildParams {
   unsigned long long* err;    // [0]: first non-finite row, [1]: first
                               // min-side excess row, [2]: max-side deficit
   double* err_val;            // [1], [2]: the offending magnitudes
+  // noise scales by value (kernel-parameter space: constant-bank operands)
+  // and RN(1/sigma) for imp_div_rcp (NaN when sigma is outside 2^+-100)
+  double sig[16];
+  double sig_rcp[16];
 };
 
 __device__ __forceinline__ int imp_max_evals(const BuildParams& P, int dim) {
@@ -232,7 +236,7 @@ struct NelderMead {
       double s = xs(slot(0), d);
 #pragma unroll
       for (int vv = 1; vv < D; ++vv) s += xs(slot(vv), d);
-      c[d] = s / D;
+      c[d] = imp_div_rcp(s, (double)D, 1.0 / D);
       xr[d] = imp_clip(c[d] + 1.0 * (c[d] - xs(sw, d)), lo[d], hi[d]);
     }
     phase = NM_REFLECT;
@@ -711,26 +715,22 @@ __device__ void imp_next_instance(const BuildParams& P, Instance& I) {
 // P(f(x) + noise in box) * sign  (abstraction.py:333-349)
 __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
                                                     const Instance& I,
-                                                    const double* x) {
+                                                    const double* x,
+                                                    const double* ndtr_tab) {
   // all 2N normal CDFs of one evaluation in one branch-free batch
   double arg[2 * IMP_N], cdf[2 * IMP_N], mean[IMP_N];
   imp_f_all(x, I.K, mean);
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) {
     const double m = mean[d];
-    const double s = P.sigma[d];
-    arg[2 * d] = imp_div(I.bhi[d] - m, s);
-    arg[2 * d + 1] = imp_div(I.blo[d] - m, s);
+    const double s = P.sig[d];
+    arg[2 * d] = imp_div_rcp(I.bhi[d] - m, s, P.sig_rcp[d]);
+    arg[2 * d + 1] = imp_div_rcp(I.blo[d] - m, s, P.sig_rcp[d]);
   }
 #ifndef IMP_NDTR_CHUNK
 #define IMP_NDTR_CHUNK 1
 #endif
-#if IMP_NDTR_CHUNK == 0
-#pragma unroll 1
-  for (int j = 0; j < 2 * IMP_N; ++j) cdf[j] = imp_ndtr(arg[j]);
-#else
-  imp_ndtr_chunks<2 * IMP_N, IMP_NDTR_CHUNK>(arg, cdf);
-#endif
+  imp_ndtr_chunks<2 * IMP_N, IMP_NDTR_CHUNK>(arg, cdf, ndtr_tab);
   double prob = 1.0;
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) prob *= cdf[2 * d] - cdf[2 * d + 1];
@@ -760,6 +760,11 @@ __device__ void imp_store_instance(const BuildParams& P, const Instance& I,
 extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
     k_refine(BuildParams P) {
   extern __shared__ double smem[];
+  __shared__ double2 s_ndtr[IMP_NDTR_TAB / 2];
+  for (int q = threadIdx.x; q < IMP_NDTR_TAB; q += blockDim.x)
+    imp_ndtr_fill_one(reinterpret_cast<double*>(s_ndtr), q);
+  __syncthreads();
+  const double* ndtr_tab = reinterpret_cast<const double*>(s_ndtr);
   constexpr int S = IMP_REFINE_BLOCK;
   NelderMead<IMP_N, S> nm;
   nm.X = smem + threadIdx.x;
@@ -801,7 +806,7 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
     if (live) {
       double p[IMP_N];
       nm.point(p);
-      double val = imp_box_objective(P, I, p);
+      double val = imp_box_objective(P, I, p, ndtr_tab);
       if (!imp_finite(val)) {
         imp_flag_nonfinite(P, I.row);
         val = 0.0;

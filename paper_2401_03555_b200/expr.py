@@ -402,7 +402,7 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
             if node[1] == "^":
                 return f"pow({a}, {b})"
             if node[1] == "/":
-                return f"imp_div({a}, {b})"
+                return _emit_div(a, b, node[3], fold, xfree)
             return f"({a} {node[1]} {b})"
         if tag == "call":
             return f"{_CUDA_FN[node[1]]}({', '.join(emit(a) for a in node[2])})"
@@ -432,10 +432,26 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
             env.update({f"w{q + 1}": disturb_reps[i][q] for q in range(p)})
             with np.errstate(all="ignore"):
                 for c, node in enumerate(folded):
-                    consts[j * n_w + i, c] = float(_eval(node, env))
+                    if node[0] == "rcp":
+                        consts[j * n_w + i, c] = _rcp(float(_eval(node[1], env)))
+                    else:
+                        consts[j * n_w + i, c] = float(_eval(node, env))
     deps = [sorted(dyn.state_dependencies(d)) for d in range(n)]
     return LoweredDynamics(source=src, n_consts=len(folded), consts=consts,
                            deps=deps)
+
+
+def _rcp(v):
+    """RN(1/v) for imp_div_rcp; NaN outside 2^+-100 (device then divides)."""
+    return 1.0 / v if 2.0 ** -100 <= abs(v) <= 2.0 ** 100 else float("nan")
+
+
+def _emit_div(a, b, bnode, fold, xfree):
+    """a / b as CUDA C, IEEE-exact: by a folded reciprocal when the divisor
+    is x-free (imp_div_rcp, no divide), else imp_div (ndtr.h)."""
+    if xfree(bnode):
+        return f"imp_div_rcp({a}, {b}, {fold(('rcp', bnode))})"
+    return f"imp_div({a}, {b})"
 
 
 def _emit_all(dyn, fold, xfree):
@@ -490,8 +506,8 @@ def _emit_all(dyn, fold, xfree):
             a, b = gen(node[2]), gen(node[3])
             if node[1] == "^":
                 s = f"pow({a}, {b})"
-            elif node[1] == "/":   # ndtr.h: IEEE divide without the 0/d slow path
-                s = f"imp_div({a}, {b})"
+            elif node[1] == "/":
+                s = _emit_div(a, b, node[3], fold, xfree)
             else:
                 s = f"({a} {node[1]} {b})"
         else:

@@ -128,7 +128,8 @@ def _eval_cuda_expr(text, x, k):
     env = {"x": x, "k": k, "sin": math.sin, "cos": math.cos,
            "tan": math.tan, "atan": math.atan, "sqrt": math.sqrt,
            "exp": math.exp, "log": math.log, "fabs": abs, "pow": math.pow,
-           "imp_min": min, "imp_max": max, "imp_div": lambda a, b: a / b}
+           "imp_min": min, "imp_max": max, "imp_div": lambda a, b: a / b,
+           "imp_div_rcp": lambda a, b, r: a / b}
     return eval(py, env)
 
 

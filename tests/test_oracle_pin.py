@@ -34,9 +34,9 @@ def ndtr_lib(tmp_path_factory):
         'extern "C" void scalar(const double* x, double* y, long n)'
         ' { for (long i = 0; i < n; ++i) y[i] = imp_ndtr(x[i]); }\n'
         'extern "C" void batch(const double* x, double* y, long n) {\n'
-        '  long i = 0;\n'
-        '  for (; i + 6 <= n; i += 6) imp_ndtr_batch<6>(x + i, y + i);\n'
-        '  for (; i < n; ++i) imp_ndtr_batch<1>(x + i, y + i); }\n'
+        '  double tab[IMP_NDTR_TAB]; imp_ndtr_fill(tab); long i = 0;\n'
+        '  for (; i + 6 <= n; i += 6) imp_ndtr_batch<6>(x + i, y + i, tab);\n'
+        '  for (; i < n; ++i) imp_ndtr_batch<1>(x + i, y + i, tab); }\n'
         'extern "C" void gexp(const double* x, double* y, long n)'
         ' { for (long i = 0; i < n; ++i) y[i] = imp_exp(x[i]); }\n')
     so = d / "ndtr_host.so"
