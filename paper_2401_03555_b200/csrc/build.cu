@@ -92,10 +92,18 @@ std::map<std::string, JitModule> g_jit_cache;
 // Threads per block of the NM kernels: the shared-memory simplex of every
 // thread ((N+1)*N + N+1 doubles) must fit in ~200 KB.
 int nm_block(int n) {
-  const size_t per = ((size_t)(n + 1) * n + (n + 1)) * sizeof(double);
+  const size_t per = ((size_t)(n + 4) * n + (n + 1)) * sizeof(double) +
+                     (64 + 16 * (size_t)n);
   int b = 128;
   while (b > 32 && b * per > 200 * 1024) b /= 2;
   return b;
+}
+
+// k_refine keeps its per-thread Instance record in shared memory (1) or in
+// registers (0)
+int inst_smem() {
+  const char* e = getenv("IMPACT_INST_SMEM");
+  return e ? atoi(e) : 0;
 }
 
 std::string config_header(const imp_build_desc* d) {
@@ -107,10 +115,12 @@ std::string config_header(const imp_build_desc* d) {
   // tuning knobs (environment overrides for experiments)
   const char* minb = getenv("IMPACT_REFINE_MINB");
   // defaults measured on the full vehicle3d / room5d builds (subsets mislead)
-  o << "#define IMP_REFINE_MINB " << (minb ? atoi(minb) : (d->n <= 8 ? 4 : 2))
+  o << "#define IMP_REFINE_MINB "
+    << (minb ? atoi(minb) : (d->n <= 4 ? 5 : d->n <= 8 ? 4 : 2))
     << "\n";
   const char* ch = getenv("IMPACT_NDTR_CHUNK");
   o << "#define IMP_NDTR_CHUNK " << (ch ? atoi(ch) : 1) << "\n";
+  o << "#define IMP_INST_SMEM " << inst_smem() << "\n";
   const char* batch = getenv("IMPACT_REFINE_BATCH");
   o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 2) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
@@ -373,7 +383,10 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     P.err_val = err_val.ptr;
 
     // --- stage 1: mean ranges -------------------------------------------------
-    const size_t nm_doubles = (size_t)(N + 1) * N + (N + 1);
+    // per-thread shared memory of the NM kernels (jit/construct.cuh:
+    // imp_nm_doubles; k_refine adds its Instance record)
+    const size_t nm_doubles = (size_t)(N + 4) * N + (N + 1);
+    const size_t inst_bytes = 5 * 8 + 5 * 4 + 4 + 2 * N * 8;
     const int block1 = nm_block(N);
     if (n_rows > 0) {
       const long long ntask = n_rows * N * 2;
@@ -422,7 +435,8 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
       P.n_items = nnz + naux + n_rows;
       instances = 2 * P.n_items;
       const int block3 = nm_block(N);
-      const size_t smem3 = block3 * nm_doubles * sizeof(double);
+      const size_t smem3 =
+          block3 * (nm_doubles * sizeof(double) + (inst_smem() ? inst_bytes : 0));
       const void* rfn = reinterpret_cast<const void*>(M.refine);
       if (smem3 > 48 * 1024)
         IMP_CUDA(cudaFuncSetAttribute(

@@ -155,14 +155,20 @@ __device__ __forceinline__ void imp_start_point(const double* lo,
 enum { NM_INIT = 0, NM_REFLECT = 1, NM_SECOND = 2, NM_SHRINK = 3 };
 enum { NM_EXPAND = 0, NM_OUTSIDE = 1, NM_INSIDE = 2 };
 
+// Shared-memory doubles per thread: D + 4 points (the D + 1 vertices, then
+// centroid, reflection and candidate -- kept out of registers so the
+// objective has room) and D + 1 vertex values.
+template <int D>
+__host__ __device__ constexpr int imp_nm_doubles() { return (D + 4) * D + D + 1; }
+
 template <int D, int S>   // S: threads per block = shared-memory stride
 struct NelderMead {
   static_assert(D + 1 <= 16, "4-bit permutation");
-  double* X;   // X[(slot * D + d) * S]
+  static constexpr int CEN = D + 1, REF = D + 2, CAND = D + 3;
+  double* X;   // X[(point * D + d) * S], points 0..D vertices, CEN, REF, CAND
   double* F;   // F[slot * S]
   unsigned long long ord;
   double lo[D], hi[D];
-  double c[D], xr[D], cand[D];
   double fr, tol, best;
   int phase, v, evals, kind, max_evals;
   bool done;
@@ -194,14 +200,10 @@ struct NelderMead {
   }
 
   __device__ __forceinline__ void point(double* p) {
-    const int sv = slot(v);
     const bool vert = phase == NM_INIT || phase == NM_SHRINK;
+    const int ps = vert ? slot(v) : (phase == NM_REFLECT ? REF : CAND);
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      double q = phase == NM_REFLECT ? xr[d] : cand[d];
-      if (vert) q = xs(sv, d);
-      p[d] = q;
-    }
+    for (int d = 0; d < D; ++d) p[d] = xs(ps, d);
   }
 
   // stable sort, termination test, centroid and reflection point
@@ -236,8 +238,9 @@ struct NelderMead {
       double s = xs(slot(0), d);
 #pragma unroll
       for (int vv = 1; vv < D; ++vv) s += xs(slot(vv), d);
-      c[d] = imp_div_rcp(s, (double)D, 1.0 / D);
-      xr[d] = imp_clip(c[d] + 1.0 * (c[d] - xs(sw, d)), lo[d], hi[d]);
+      const double cd = imp_div_rcp(s, (double)D, 1.0 / D);
+      xs(CEN, d) = cd;
+      xs(REF, d) = imp_clip(cd + 1.0 * (cd - xs(sw, d)), lo[d], hi[d]);
     }
     phase = NM_REFLECT;
   }
@@ -260,15 +263,15 @@ struct NelderMead {
         const double coef = kind == NM_EXPAND ? 2.0 : 0.5;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          const double w = xs(sw, d);
-          const double dir = kind == NM_EXPAND ? c[d] - w
-                             : (kind == NM_OUTSIDE ? xr[d] - c[d] : w - c[d]);
-          cand[d] = imp_clip(c[d] + coef * dir, lo[d], hi[d]);
+          const double w = xs(sw, d), cd = xs(CEN, d);
+          const double dir = kind == NM_EXPAND ? cd - w
+                             : (kind == NM_OUTSIDE ? xs(REF, d) - cd : w - cd);
+          xs(CAND, d) = imp_clip(cd + coef * dir, lo[d], hi[d]);
         }
         phase = NM_SECOND;
       } else {
 #pragma unroll
-        for (int d = 0; d < D; ++d) xs(sw, d) = xr[d];
+        for (int d = 0; d < D; ++d) xs(sw, d) = xs(REF, d);
         fs(sw) = fr;
         iter = true;
       }
@@ -279,8 +282,9 @@ struct NelderMead {
                         (kind == NM_OUTSIDE ? fp < fr : fp < fs(sw));
       if (take) {
         const bool use_c = kind != NM_EXPAND || fp < fr;
+        const int from = use_c ? CAND : REF;
 #pragma unroll
-        for (int d = 0; d < D; ++d) xs(sw, d) = use_c ? cand[d] : xr[d];
+        for (int d = 0; d < D; ++d) xs(sw, d) = xs(from, d);
         fs(sw) = use_c ? fp : fr;
         iter = true;
       } else {
@@ -329,7 +333,7 @@ __device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
   } else {
     NelderMead<D, IMP_MEAN_BLOCK> nm;
     nm.X = smem;
-    nm.F = smem + (D + 1) * D * S;
+    nm.F = smem + (D + 4) * D * S;
     nm.tol = P.tol;
     nm.max_evals = imp_max_evals(P, D);
 #pragma unroll
@@ -623,31 +627,29 @@ extern "C" __global__ void k_outer(BuildParams P) {
 // Stage 3: coupled refinement, one thread per NM instance
 // ---------------------------------------------------------------------------
 
+// One per thread, in shared memory (AoS: the 8-byte fields of a warp fall on
+// distinct banks for the sizes that occur); registers stay for the objective.
 struct Instance {
-  long long row, rel;          // row, item index within the row
-  long long nt, nx;            // live t entries / aux items of the row
+  long long row;               // row
   long long t0, x0;            // CSR / aux offsets of the row
+  long long slot;              // CSR / aux index
+  const double* K;             // folded dynamics constants of the row
+  int rel;                     // item index within the row
+  int nt, nx;                  // live t entries / aux items of the row
   int sgn;
-  int kind;          // 0: t entry, 1: aux (target/avoid), 2: cover
-  long long slot;    // CSR / aux index
+  int kind;                    // 0: t entry, 1: aux (target/avoid), 2: cover
   double blo[IMP_N], bhi[IMP_N];
-  double clo[IMP_N], chi[IMP_N];
-  const double* K;
 };
+static_assert(sizeof(Instance) == 64 + 16 * IMP_N, "build.cu inst_bytes");
 
 __device__ void imp_load_row(const BuildParams& P, Instance& I) {
   const long long r = I.row;
   I.t0 = P.row_ptr[r];
-  I.nt = P.row_ptr[r + 1] - I.t0;
+  I.nt = (int)(P.row_ptr[r + 1] - I.t0);
   I.x0 = P.aux_ptr[r];
-  I.nx = P.aux_ptr[r + 1] - I.x0;
+  I.nx = (int)(P.aux_ptr[r + 1] - I.x0);
   int k, j, i;
   imp_row_kji(P, r, k, j, i);
-#pragma unroll
-  for (int d = 0; d < IMP_N; ++d) {
-    I.clo[d] = P.src_lo[(long long)k * IMP_N + d];
-    I.chi[d] = P.src_hi[(long long)k * IMP_N + d];
-  }
   I.K = P.consts + (long long)(j * P.n_w + i) * IMP_NC;
 }
 
@@ -680,6 +682,19 @@ __device__ void imp_load_item(const BuildParams& P, Instance& I) {
   }
 }
 
+// Source cell of a row: the NM box (clipped cell of the row's state k).
+__device__ __forceinline__ void imp_source_cell(const BuildParams& P,
+                                                long long r, double* lo,
+                                                double* hi) {
+  int k, j, i;
+  imp_row_kji(P, r, k, j, i);
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) {
+    lo[d] = P.src_lo[(long long)k * IMP_N + d];
+    hi[d] = P.src_hi[(long long)k * IMP_N + d];
+  }
+}
+
 // Instance g = 2 * item + sign; items of row r are its live t entries, then
 // its live target / avoid boxes, then the cover box.
 __device__ void imp_seek_instance(const BuildParams& P, long long g,
@@ -694,7 +709,7 @@ __device__ void imp_seek_instance(const BuildParams& P, long long g,
   }
   I.row = lo;
   imp_load_row(P, I);
-  I.rel = item - (I.t0 + I.x0 + I.row);
+  I.rel = (int)(item - (I.t0 + I.x0 + I.row));
   imp_load_item(P, I);
 }
 
@@ -768,7 +783,13 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
   constexpr int S = IMP_REFINE_BLOCK;
   NelderMead<IMP_N, S> nm;
   nm.X = smem + threadIdx.x;
-  nm.F = smem + (IMP_N + 1) * IMP_N * S + threadIdx.x;
+  nm.F = smem + (IMP_N + 4) * IMP_N * S + threadIdx.x;
+#if IMP_INST_SMEM
+  Instance& I = reinterpret_cast<Instance*>(smem + imp_nm_doubles<IMP_N>() * S)
+      [threadIdx.x];
+#else
+  Instance I;
+#endif
   nm.tol = P.tol;
   nm.max_evals = imp_max_evals(P, IMP_N);
   const int ms = imp_multistart(P, IMP_N);
@@ -781,16 +802,11 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
   long long g = (long long)atomicAdd(counter, (unsigned long long)B);
   long long g_end = min(total, g + B);
   if (g >= total) return;
-  Instance I;
   imp_seek_instance(P, g, I);
-#pragma unroll
-  for (int d = 0; d < IMP_N; ++d) {
-    nm.lo[d] = I.clo[d];
-    nm.hi[d] = I.chi[d];
-  }
+  imp_source_cell(P, I.row, nm.lo, nm.hi);
   int s = 0;
   double best = IMP_INF;
-  unsigned long long ev = 0;
+  unsigned int ev = 0, slots = 0;   // per thread: far below 2^32
   {
     double st[IMP_N];
     imp_start_point<IMP_N>(nm.lo, nm.hi, 0, st);
@@ -800,7 +816,6 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
   // is a nested branch that reconverges before the next evaluation, so a
   // warp never splits into groups evaluating the objective separately.
   bool live = true;
-  unsigned long long slots = 0;
   while (__any_sync(__activemask(), live)) {
     ++slots;
     if (live) {
@@ -829,11 +844,7 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
           if (!more) {
             live = false;
           } else {
-#pragma unroll
-            for (int d = 0; d < IMP_N; ++d) {
-              nm.lo[d] = I.clo[d];
-              nm.hi[d] = I.chi[d];
-            }
+            imp_source_cell(P, I.row, nm.lo, nm.hi);
             s = 0;
             best = IMP_INF;
           }
@@ -847,8 +858,8 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
     }
     __syncwarp(__activemask());
   }
-  atomicAdd((unsigned long long*)P.evals, ev);
-  atomicAdd((unsigned long long*)P.evals + 1, slots);
+  atomicAdd((unsigned long long*)P.evals, (unsigned long long)ev);
+  atomicAdd((unsigned long long*)P.evals + 1, (unsigned long long)slots);
 }
 
 
