@@ -168,3 +168,34 @@ def synthesize(m, spec, mode="pessimistic", eps=1e-6, horizon=None,
     return dict(p_min=p_min, p_max=p_max, policy=ph1.policy,
                 iterations=(ph1.iterations, ph2.iterations),
                 fallback=(ph1.fallback, ph2.fallback), phase1=ph1, phase2=ph2)
+
+
+def diagnose(m, spec="reach", mode="pessimistic", eps=1e-6,
+             max_iterations=10**6):
+    """diagnose_convergence (synthesis.py:321-361): each phase-1 bound
+    iterated on its own until its own step drops to eps -> (k0, k1)."""
+    if spec == "safety":
+        lp = "max" if mode == "pessimistic" else "min"
+        u_obj = "min"
+    else:
+        lp = "min" if mode == "pessimistic" else "max"
+        u_obj = "max"
+    rows = phase_rows(m, stacked(m))
+    v0 = np.zeros(m.n_s)
+    v1 = np.ones(m.n_s)
+    k0 = k1 = None
+    for it in range(1, max_iterations + 1):
+        if k0 is None:
+            n0, _ = bellman(m, v0, lp, u_obj, spec, rows=rows)
+            if np.max(np.abs(n0 - v0)) <= eps:
+                k0 = it
+            v0 = n0
+        if k1 is None:
+            n1, _ = bellman(m, v1, lp, u_obj, spec, rows=rows)
+            if np.max(np.abs(n1 - v1)) <= eps:
+                k1 = it
+            v1 = n1
+        if k0 is not None and k1 is not None:
+            return report_k(k0), report_k(k1)
+    raise ConvergenceError(f"no self-convergence within {max_iterations} "
+                           "iterations", k0=report_k(k0), k1=report_k(k1))

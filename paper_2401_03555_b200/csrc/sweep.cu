@@ -24,6 +24,8 @@
 #include <cuda_pipeline.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -172,7 +174,15 @@ struct SweepArgs {
   // gets never depends on its shard or neighbours)
   const int* list;
   int64_t n_list;
-  int* hint;            // (2 * n_phase_rows) warm-start crossing entries
+  // when set, the list length lives on the device (rows the streaming
+  // verify pass could not settle, appended during the same iteration)
+  const unsigned long long* n_list_dev;
+  unsigned long long* miss_cnt;   // streaming pass: miss counter of the class
+  int* miss_list;                 // streaming pass: miss rows of the class
+  int* hint;            // (2 * n_phase_rows) warm-start crossing columns
+  int verify_hint;      // search kernel: try the hint before searching
+  const int* perm0;     // columns by rank (hint publication)
+  const int* perm1;
   double* out0;
   double* out1;
 };
@@ -230,17 +240,28 @@ __device__ __forceinline__ double2 team_sum2(double x, double y,
   }
 }
 
+// A row's value from its team-reduced sums (both K5 kernels use exactly
+// this expression): lower mass + filled head below the crossing rank P +
+// the partial fill of slot P.
+__device__ __forceinline__ double row_value(double lw, double f, double s,
+                                            double c, int p, int n,
+                                            const double* ws) {
+  const double x = p < n ? fma(s - c, __ldg(ws + p), f) : f;
+  return lw + x;
+}
+
 // One row per team.  TEAM threads hold up to TEAM*EPT stored entries in
 // registers (missing entries padded with h = 0, rank = +inf, so every loop
 // is unguarded and the per-lane sums do not depend on EPT); the two
 // virtual slots (target, avoid) live in team thread 0.
 //
-// Warm start: `hint` keeps, per phase row and track, the row-local index of
-// last sweep's crossing entry (-1: no crossing, -2: unknown).  Near
-// convergence the global order barely moves, so the guess usually verifies
-// with one two-sided probe; otherwise the binary search runs.  Either way
-// the value is computed from C(<P*) with the same reduction, so the result
-// is independent of the hint (bitwise).
+// Warm start: `hint` keeps, per phase row and track, the column of last
+// sweep's crossing slot (-1: no crossing, -2: unknown).  Near convergence
+// the global order barely moves, so the column's new rank usually verifies
+// with one two-sided probe (k_sweep_stream, below); otherwise the binary
+// search here runs.  Either way the value is computed from C(<P*) with the
+// same per-lane order and team tree, so the result is independent of the
+// hint and of which kernel settled the row (bitwise).
 // i-th row of this launch's class list: phase row t, CSR row, start,
 // length; team-uniform.
 __device__ __forceinline__ void class_row(const SweepArgs& a, int64_t i,
@@ -294,14 +315,15 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     __pipeline_commit();
   };
 
+  const int64_t n_list = a.n_list_dev ? (int64_t)*a.n_list_dev : a.n_list;
   int64_t row = 0, beg = 0, t = 0;
   int m = 0;
   int64_t i = team0;
-  if (i < a.n_list) class_row(a, i, t, row, beg, m);
+  if (i < n_list) class_row(a, i, t, row, beg, m);
   if constexpr (STAGED) {
-    if (i < a.n_list) issue(beg, m);
+    if (i < n_list) issue(beg, m);
   }
-  while (i < a.n_list) {
+  while (i < n_list) {
     double h[EPT];
     RankReg<WIDE> rk[EPT];
     double lw0 = 0.0, lw1 = 0.0;
@@ -331,15 +353,15 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
         }
         h[e] = u - l;
         const double2 w = __ldg(a.colw + c);
-        lw0 += l * w.x;
-        lw1 += l * w.y;
+        lw0 = fma(l, w.x, lw0);
+        lw1 = fma(l, w.y, lw1);
         rk[e].load(a, c);
       }
     }
     if constexpr (STAGED) {
-      if (i_n < a.n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
+      if (i_n < n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
       team_sync();                           // stage consumed
-      if (i_n < a.n_list) issue(beg_n, m_n);
+      if (i_n < n_list) issue(beg_n, m_n);
     }
     // virtual slots n_s (target) and n_s + 1 (avoid) on team thread 0
     double hv[2] = {0.0, 0.0};
@@ -351,8 +373,8 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
       hv[0] = a.r_max[row] - lr;
       hv[1] = a.a_max[row] - la;
       const double2 wr = __ldg(a.colw + a.n_s), wa = __ldg(a.colw + a.n_s + 1);
-      lw0 += lr * wr.x + la * wa.x;
-      lw1 += lr * wr.y + la * wa.y;
+      lw0 = fma(la, wa.x, fma(lr, wr.x, lw0));
+      lw1 = fma(la, wa.y, fma(lr, wr.y, lw1));
       rv[0].load(a, a.n_s);
       rv[1].load(a, a.n_s + 1);
     }
@@ -378,17 +400,15 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
 
     // warm start: rank of last sweep's crossing entry
     int g0 = -2, g1 = -2;
-    if (a.hint) {
+    if (a.hint && a.verify_hint) {
       const int hq[2] = {a.hint[2 * t], a.hint[2 * t + 1]};
       int gr[2];
 #pragma unroll
       for (int o = 0; o < 2; ++o) {
         gr[o] = hq[o];
         if (hq[o] >= 0) {
-          const int c = hq[o] < m ? __ldg(a.col + beg + hq[o])
-                                  : a.n_s + (hq[o] - m);
           RankReg<WIDE> r;
-          r.load(a, c);
+          r.load(a, hq[o]);
           gr[o] = o ? r.r1() : r.r0();
         } else if (hq[o] == -1) {
           gr[o] = a.n;          // "no crossing": verify C(<n) < s
@@ -425,43 +445,32 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     }
     // filled part: sum_{rank<P} head * w, weights regathered by rank
     double f0 = 0.0, f1 = 0.0;
-    int e0 = -1, e1 = -1;   // row-local index of the crossing entry
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const int r0 = rk[e].r0(), r1 = rk[e].r1();
-      if (r0 < p0) f0 += h[e] * __ldg(a.ws0 + r0);
-      if (r1 < p1) f1 += h[e] * __ldg(a.ws1 + r1);
-      if (r0 == p0) e0 = e * TEAM + tid;
-      if (r1 == p1) e1 = e * TEAM + tid;
+      if (r0 < p0) f0 = fma(h[e], __ldg(a.ws0 + r0), f0);
+      if (r1 < p1) f1 = fma(h[e], __ldg(a.ws1 + r1), f1);
     }
     if (tid == 0) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int r0 = rv[v].r0(), r1 = rv[v].r1();
-        if (r0 < p0) f0 += hv[v] * __ldg(a.ws0 + r0);
-        if (r1 < p1) f1 += hv[v] * __ldg(a.ws1 + r1);
-        if (r0 == p0) e0 = m + v;
-        if (r1 == p1) e1 = m + v;
+        if (r0 < p0) f0 = fma(hv[v], __ldg(a.ws0 + r0), f0);
+        if (r1 < p1) f1 = fma(hv[v], __ldg(a.ws1 + r1), f1);
       }
     }
     const double2 lw = team_sum2<TEAM>(lw0, lw1, part, parity);
     const double2 g = team_sum2<TEAM>(f0, f1, part, parity);
-    if (a.hint) {
-      // publish the crossing entries (exactly one thread holds each)
-      if (p0 >= a.n && tid == 0) a.hint[2 * t] = -1;
-      else if (e0 >= 0) a.hint[2 * t] = e0;
-      if (p1 >= a.n && tid == 0) a.hint[2 * t + 1] = -1;
-      else if (e1 >= 0) a.hint[2 * t + 1] = e1;
-    }
     if (tid == 0) {
-      double x0 = g.x, x1 = g.y;
-      if (p0 < a.n) x0 += (s - c0) * a.ws0[p0];
-      if (p1 < a.n) x1 += (s - c1) * a.ws1[p1];
-      a.out0[t] = lw.x + x0;
-      a.out1[t] = lw.y + x1;
+      if (a.hint) {   // publish the crossing columns (ws index = rank)
+        a.hint[2 * t] = p0 >= a.n ? -1 : __ldg(a.perm0 + p0);
+        a.hint[2 * t + 1] = p1 >= a.n ? -1 : __ldg(a.perm1 + p1);
+      }
+      a.out0[t] = row_value(lw.x, g.x, s, c0, p0, a.n, a.ws0);
+      a.out1[t] = row_value(lw.y, g.y, s, c1, p1, a.n, a.ws1);
     }
     if constexpr (!STAGED) {
-      if (i_n < a.n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
+      if (i_n < n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
     }
     i = i_n;
     t = t_n;
@@ -471,6 +480,136 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
   }
 }
 
+
+// Team sum of K values with exactly team_sum2's tree per value (warp xor
+// butterfly; CTA teams: warp partials -> shared memory -> every warp
+// re-reduces the NW partials), so the streaming pass reproduces the search
+// kernel's sums bit for bit.
+template <int TEAM, int K>
+__device__ __forceinline__ void team_sum_k(double* v, double* part) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  if constexpr (TEAM > 32) {
+    constexpr int NW = TEAM / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) part[k * NW + warp] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      v[k] = warp_sum(lane < NW ? part[k * NW + lane] : 0.0);
+    __syncthreads();   // part is reused by the team's next row
+  }
+}
+
+// K5a, streaming verify pass: one read of the row settles it when last
+// sweep's crossing column still marks the crossing in the new order.  Per
+// lane, in the search kernel's entry order (q = e * TEAM + tid), it
+// accumulates  sum l*w,  C(<g), C(<g+1) and  sum_{rank<g} h*w  for both
+// tracks (g = the hinted column's new rank); nothing is kept in registers
+// across entries, so the pass runs at low register count and high
+// occupancy.  Rows whose guess fails (or is unknown) are appended to the
+// class's miss list and priced by k_sweep (binary search) right after.
+template <int TEAM, bool WIDE>
+__global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
+                                  TEAM == 32 ? 4 : 1024 / TEAM)
+    k_sweep_stream(SweepArgs a) {
+  if (a.ctl && a.ctl->done) return;
+  constexpr int NW = TEAM > 32 ? TEAM / 32 : 1;
+  constexpr int U = 4;   // entries in flight per lane
+  __shared__ double part[8 * NW];
+  const int tid = TEAM == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  const int64_t team0 = TEAM == 32
+      ? (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)
+      : (int64_t)blockIdx.x;
+  const int64_t nteams = TEAM == 32
+      ? (int64_t)gridDim.x * (blockDim.x >> 5) : (int64_t)gridDim.x;
+  for (int64_t i = team0; i < a.n_list; i += nteams) {
+    const int64_t t = a.list[i];
+    const int64_t row = phase_row(a, t);
+    const int64_t beg = a.row_ptr[row];
+    const int m = (int)(a.row_ptr[row + 1] - beg);
+    const double s = a.slack[row];
+    const bool zero = !(s > 0.0);   // nothing filled: P = 0, C = 0
+    int g0 = 0, g1 = 0;
+    if (!zero) {
+      const int h0 = a.hint[2 * t], h1 = a.hint[2 * t + 1];
+      if (h0 < -1 || h1 < -1) {     // unknown (first sweep): search
+        if (tid == 0) a.miss_list[atomicAdd(a.miss_cnt, 1ull)] = (int)t;
+        continue;
+      }
+      RankReg<WIDE> r;
+      if (h0 >= 0) { r.load(a, h0); g0 = r.r0(); } else g0 = a.n;
+      if (h1 >= 0) { r.load(a, h1); g1 = r.r1(); } else g1 = a.n;
+    }
+    // v: lw0 lw1 | C(<g) 0 1 | C(<g+1) 0 1 | F(<g) 0 1
+    double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const int32_t* colp = a.col + beg;
+    const double* lop = a.lo + beg;
+    const double* hip = a.hi + beg;
+    for (int q = tid; q < m; q += U * TEAM) {
+      int c[U];
+      double l[U], u[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int qq = q + k * TEAM;
+        c[k] = -1;
+        l[k] = u[k] = 0.0;
+        if (qq < m) {
+          c[k] = __ldcs(colp + qq);
+          l[k] = __ldcs(lop + qq);
+          u[k] = __ldcs(hip + qq);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (c[k] >= 0) {
+          const double2 w = __ldg(a.colw + c[k]);
+          RankReg<WIDE> rk;
+          rk.load(a, c[k]);
+          const double h = u[k] - l[k];
+          v[0] = fma(l[k], w.x, v[0]);
+          v[1] = fma(l[k], w.y, v[1]);
+          const int r0 = rk.r0(), r1 = rk.r1();
+          if (r0 < g0) { v[2] += h; v[6] = fma(h, w.x, v[6]); }
+          if (r1 < g1) { v[3] += h; v[7] = fma(h, w.y, v[7]); }
+          if (r0 <= g0) v[4] += h;
+          if (r1 <= g1) v[5] += h;
+        }
+      }
+    }
+    if (tid == 0) {   // virtual slots n_s (target) and n_s + 1 (avoid)
+      const double lr = a.r_min[row], la = a.a_min[row];
+      const double hv[2] = {a.r_max[row] - lr, a.a_max[row] - la};
+      const double2 wv[2] = {__ldg(a.colw + a.n_s), __ldg(a.colw + a.n_s + 1)};
+      v[0] = fma(la, wv[1].x, fma(lr, wv[0].x, v[0]));
+      v[1] = fma(la, wv[1].y, fma(lr, wv[0].y, v[1]));
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        RankReg<WIDE> rk;
+        rk.load(a, a.n_s + o);
+        const int r0 = rk.r0(), r1 = rk.r1();
+        if (r0 < g0) { v[2] += hv[o]; v[6] = fma(hv[o], wv[o].x, v[6]); }
+        if (r1 < g1) { v[3] += hv[o]; v[7] = fma(hv[o], wv[o].y, v[7]); }
+        if (r0 <= g0) v[4] += hv[o];
+        if (r1 <= g1) v[5] += hv[o];
+      }
+    }
+    team_sum_k<TEAM, 8>(v, part);
+    const bool ok0 = zero || (v[2] < s && (g0 >= a.n || v[4] >= s));
+    const bool ok1 = zero || (v[3] < s && (g1 >= a.n || v[5] >= s));
+    if (tid == 0) {
+      if (ok0 && ok1) {
+        a.out0[t] = row_value(v[0], v[6], s, v[2], g0, a.n, a.ws0);
+        a.out1[t] = row_value(v[1], v[7], s, v[3], g1, a.n, a.ws1);
+      } else {
+        a.miss_list[atomicAdd(a.miss_cnt, 1ull)] = (int)t;
+      }
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Robust Bellman reduction + convergence statistics
@@ -679,6 +818,9 @@ struct Work {
   static constexpr int NCLASS = 8;
   DevBuf<int> class_rows;
   DevBuf<unsigned long long> class_cnt;   // counts, then scatter cursors
+  DevBuf<int> miss_rows;                  // K5a misses, class-partitioned
+  DevBuf<unsigned long long> miss_cnt;    // per class
+  DevBuf<unsigned long long> miss_total;  // IMP_SWEEP_STATS: misses, sweeps
   int64_t class_off[NCLASS + 1] = {};
   bool classes_all = false;   // class lists hold the unfixed phase
 
@@ -702,6 +844,10 @@ struct Work {
     IMP_CUDA(cudaMemset(hint.ptr, 0xfe, hint.bytes()));   // -2: unknown
     class_rows.alloc(std::max<int64_t>(phase_rows, 1));
     class_cnt.alloc(2 * NCLASS);
+    miss_rows.alloc(std::max<int64_t>(phase_rows, 1));
+    miss_cnt.alloc(NCLASS);
+    miss_total.alloc(2);
+    IMP_CUDA(cudaMemset(miss_total.ptr, 0, miss_total.bytes()));
     colw.alloc(n);
     rank.alloc(n);
     if (!wide) rank16.alloc(n);
@@ -798,6 +944,35 @@ struct Team {
   int team, ept;
 };
 
+// IMP_SWEEP_STATS=1: per-iteration K5a miss counts accumulate on the
+// device (one extra tiny launch per iteration) and imp_run_phase prints
+// the miss rate to stderr.
+bool sweep_stats() {
+  static const int on = [] {
+    const char* e = getenv("IMP_SWEEP_STATS");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return on != 0;
+}
+
+__global__ void k_miss_accum(const Ctl* ctl, const unsigned long long* cnt,
+                             int nclass, unsigned long long* total) {
+  if (ctl && ctl->done) return;
+  unsigned long long m = 0;
+  for (int c = 0; c < nclass; ++c) m += cnt[c];
+  total[0] += m;
+  total[1] += 1;
+}
+
+// IMP_SWEEP_STREAM=0 disables K5a (search kernel only), for A/B timing.
+bool stream_disabled() {
+  static const int off = [] {
+    const char* e = getenv("IMP_SWEEP_STREAM");
+    return e && e[0] == '0' ? 1 : 0;
+  }();
+  return off != 0;
+}
+
 Team choose_team(int max_row) {
   const int need = std::max(max_row, 1);
   for (int e : {1, 2, 4, 8, 16})
@@ -833,6 +1008,33 @@ void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
 }
 
 
+template <int TEAM, bool WIDE>
+void launch_stream_t(const SweepArgs& a, int sms, cudaStream_t s) {
+  auto kern = k_sweep_stream<TEAM, WIDE>;
+  const int threads = TEAM == 32 ? 256 : TEAM;
+  int per_sm = 0;
+  IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                         threads, 0));
+  per_sm = std::max(per_sm, 1);
+  const int64_t teams_per_block = TEAM == 32 ? threads / 32 : 1;
+  const int64_t need = (a.n_list + teams_per_block - 1) / teams_per_block;
+  const int blocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>(need, (int64_t)sms * per_sm));
+  kern<<<blocks, threads, 0, s>>>(a);
+  IMP_CUDA(cudaGetLastError());
+}
+
+template <bool WIDE>
+void launch_stream_w(const SweepArgs& a, int team, int sms, cudaStream_t s) {
+  switch (team) {
+    case 32: return launch_stream_t<32, WIDE>(a, sms, s);
+    case 64: return launch_stream_t<64, WIDE>(a, sms, s);
+    case 128: return launch_stream_t<128, WIDE>(a, sms, s);
+    case 256: return launch_stream_t<256, WIDE>(a, sms, s);
+    default: return launch_stream_t<512, WIDE>(a, sms, s);
+  }
+}
+
 template <bool WIDE>
 void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
   switch (tm.team) {
@@ -861,19 +1063,57 @@ void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
 //               adds +0.0 and does not change any sum)
 //   CTA teams   m <= 2048 / 4096 / 8192 / 16384 (128 / 256 / 512 / 512x32)
 // Returns the number of launches.
+//
+// With warm-start hints (phase loops), every class first runs the
+// streaming verify pass K5a (k_sweep_stream), which settles the rows whose
+// crossing column carried over from the last sweep and appends the rest to
+// the class's miss list; then the search kernel K5b (k_sweep) prices the
+// misses, with the list length read on the device (graph-capturable, no
+// host sync).  Both kernels produce identical bits for a row.
 int launch_sweep(SweepArgs sa, const Work& w, bool wide, int sms,
                  cudaStream_t s) {
   static const int teams[] = {32, 32, 32, 32, 128, 256, 512, 512};
   static const int epts[] = {4, 8, 12, 16, 16, 16, 16, 32};
   int launches = 0;
+  const bool two_pass = sa.hint != nullptr && !stream_disabled();
+  if (two_pass) {
+    IMP_CUDA(cudaMemsetAsync(w.miss_cnt.ptr, 0, w.miss_cnt.bytes(), s));
+    for (int c = 0; c < Work::NCLASS; ++c) {
+      const int64_t cnt = w.class_off[c + 1] - w.class_off[c];
+      if (cnt == 0) continue;
+      SweepArgs a = sa;
+      a.list = w.class_rows.ptr + w.class_off[c];
+      a.n_list = cnt;
+      a.miss_cnt = w.miss_cnt.ptr + c;
+      a.miss_list = w.miss_rows.ptr + w.class_off[c];
+      if (wide) launch_stream_w<true>(a, teams[c], sms, s);
+      else launch_stream_w<false>(a, teams[c], sms, s);
+      ++launches;
+    }
+  }
   for (int c = 0; c < Work::NCLASS; ++c) {
     const int64_t cnt = w.class_off[c + 1] - w.class_off[c];
     if (cnt == 0) continue;
-    sa.list = w.class_rows.ptr + w.class_off[c];
-    sa.n_list = cnt;
+    SweepArgs a = sa;
+    if (two_pass) {
+      a.list = w.miss_rows.ptr + w.class_off[c];
+      a.n_list = cnt;                        // grid bound; true count below
+      a.n_list_dev = w.miss_cnt.ptr + c;
+      a.verify_hint = 0;                     // K5a already tried it
+    } else {
+      a.list = w.class_rows.ptr + w.class_off[c];
+      a.n_list = cnt;
+      a.verify_hint = sa.hint != nullptr;
+    }
     Team tm{teams[c], epts[c]};
-    if (wide) launch_sweep_w<true>(sa, tm, sms, s);
-    else launch_sweep_w<false>(sa, tm, sms, s);
+    if (wide) launch_sweep_w<true>(a, tm, sms, s);
+    else launch_sweep_w<false>(a, tm, sms, s);
+    ++launches;
+  }
+  if (two_pass && sweep_stats()) {
+    k_miss_accum<<<1, 1, 0, s>>>(sa.ctl, w.miss_cnt.ptr, Work::NCLASS,
+                                 w.miss_total.ptr);
+    IMP_CUDA(cudaGetLastError());
     ++launches;
   }
   return launches;
@@ -964,6 +1204,8 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   sa.out0 = w.val[0].ptr;
   sa.out1 = w.val[1].ptr;
   sa.hint = w.hint.ptr;
+  sa.perm0 = w.perm[0].ptr;
+  sa.perm1 = w.perm[1].ptr;
   const int n_sweep = launch_sweep(sa, w, w.wide, L.sms, s);
   w.last_sweep = sa;
 
@@ -1097,6 +1339,17 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
 
+    if (sweep_stats()) {
+      unsigned long long mt[2];
+      IMP_CUDA(cudaMemcpy(mt, w.miss_total.ptr, sizeof(mt),
+                          cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[imp] phase: %lld iterations, %lld rows, K5a misses "
+              "%llu of %llu row sweeps (%.2f%%), %.3f ms/iteration\n",
+              hc.it, (long long)phase_rows, mt[0],
+              mt[1] * (unsigned long long)phase_rows,
+              mt[1] ? 100.0 * mt[0] / (double)(mt[1] * phase_rows) : 0.0,
+              hc.it ? ms / hc.it : 0.0);
+    }
     const int cur = hc.cur;
     if (out->v0)
       IMP_CUDA(cudaMemcpy(out->v0, w.v[0][cur].ptr, sizeof(double) * h->n_s,

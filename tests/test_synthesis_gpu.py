@@ -308,3 +308,84 @@ def test_shard_sweeps_bitwise_equal_single_handle(name):
             gpick.append(pol.cpu().numpy())
         assert np.array_equal(np.concatenate(got), want)
         assert np.array_equal(np.concatenate(gpick), wpick)
+
+
+# --- optimistic mode, finite horizon, diagnose_convergence
+# as first-class flags of the same device loop, against the oracle ----------
+
+def _mini_case(name):
+    if not G.have("full_" + name):
+        pytest.skip("fixture not generated")
+    g = G.load("full_" + name)
+    cfg = G.config_of(g)
+    return cfg, G.imdp(g), G.model(g), G.spec_of(cfg)
+
+
+def _gpu_synth(m, spec, **kw):
+    if m.input_space is None:
+        return verify(m, spec=spec, **kw)
+    if spec == "safety":
+        return synthesize_safe(m, **kw)
+    return synthesize_reach(m, **kw)
+
+
+def _check_against_oracle(c, want, m, spec):
+    assert tuple(c.meta["iterations"]) == tuple(want["iterations"])
+    assert tuple(c.meta["fallback"]) == tuple(want["fallback"])
+    assert np.max(np.abs(c.p_min - want["p_min"])) <= TOL
+    assert np.max(np.abs(c.p_max - want["p_max"])) <= TOL
+    if c.policy is not None:
+        # margin-aware policy rule: where the inputs differ,
+        # the GPU's must be eps-optimal under the oracle's phase-1 values
+        diff = np.flatnonzero(c.policy != want["policy"])
+        if len(diff):
+            lp = "min" if spec == "reach" else "max"
+            if c.meta["mode"] == "optimistic":
+                lp = "max" if lp == "min" else "min"
+            u_obj = "max" if spec == "reach" else "min"
+            om = oracle_model(m)
+            v0 = want["phase1"].v0
+            ref, _ = ORI.bellman(om, v0, lp, u_obj, spec, want["policy"])
+            alt, _ = ORI.bellman(om, v0, lp, u_obj, spec, c.policy)
+            assert np.max(np.abs(ref - alt)) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["robot2d_ra_mini", "room5d_mini",
+                                  "vehicle3d_mini", "bas4d_mini"])
+def test_optimistic_mode_matches_oracle(name):
+    cfg, m, om, spec = _mini_case(name)
+    c = _gpu_synth(m, spec, mode="optimistic", eps=1e-6)
+    want = ORI.synthesize(om, spec, mode="optimistic", eps=1e-6)
+    _check_against_oracle(c, want, m, spec)
+
+
+@pytest.mark.parametrize("name", ["robot2d_ra_mini", "room5d_mini",
+                                  "bas4d_mini"])
+@pytest.mark.parametrize("horizon", [1, 3, 10])
+def test_finite_horizon_matches_oracle(name, horizon):
+    cfg, m, om, spec = _mini_case(name)
+    c = _gpu_synth(m, spec, horizon=horizon)
+    want = ORI.synthesize(om, spec, horizon=horizon)
+    assert c.meta["horizon"] == horizon
+    _check_against_oracle(c, want, m, spec)
+
+
+@pytest.mark.parametrize("name", ["robot2d_ra_mini", "room5d_mini",
+                                  "vehicle3d_mini", "bas4d_mini",
+                                  "bas7d_mini"])
+@pytest.mark.parametrize("mode", ["pessimistic", "optimistic"])
+def test_diagnose_convergence_matches_oracle(name, mode):
+    cfg, m, om, spec = _mini_case(name)
+    got = diagnose_convergence(m, spec=spec, mode=mode, eps=1e-6)
+    assert got == ORI.diagnose(om, spec=spec, mode=mode, eps=1e-6)
+
+
+def test_diagnose_convergence_cap_reports_partial_horizons():
+    """dim6 (0.8 x contraction, like dim14) does not self-converge within a
+    short cap: ConvergenceError carries the same k0 / k1 as the oracle."""
+    cfg, m, om, spec = _mini_case("dim6_mini")
+    with pytest.raises(ConvergenceError) as got:
+        diagnose_convergence(m, spec=spec, eps=1e-6, max_iterations=60)
+    with pytest.raises(ConvergenceError) as want:
+        ORI.diagnose(om, spec=spec, eps=1e-6, max_iterations=60)
+    assert (got.value.k0, got.value.k1) == (want.value.k0, want.value.k1)
