@@ -236,6 +236,30 @@ int imp_fp64_peak(int device, double* gflops);
 int imp_time_sweep(imp_imdp* h, int32_t spec, int32_t lp, int32_t reps,
                    double* ms);
 
+/* ---------------------------------------------------------------------- */
+/* Text export in the reference's file formats (fileio.py)                 */
+/* ---------------------------------------------------------------------- */
+
+/* Dense text lines of rows [row_begin, row_end) of t_min (which = 0) or
+ * t_max (which = 1), exactly as the reference's save_matrix writes them
+ * (fileio.py:94-101: format(x, ".17g") per field, one space between fields,
+ * '\n' per row; the header line is the caller's).  Rendered on the device
+ * from the sparse rows, zeros included.  buf == NULL: size query only
+ * (*out_len = bytes needed).  Replaces the per-row Python formatting loop
+ * of fileio.save_matrix / save_abstraction (:285-299). */
+int imp_export_text_rows(const imp_imdp* h, int32_t which, int64_t row_begin,
+                         int64_t row_end, char* buf, int64_t cap,
+                         int64_t* out_len);
+
+/* Text body of n host doubles as lines of `cols` fields (row-major; n a
+ * multiple of cols): format(x, ".17g"), ' ' between fields, '\n' after each
+ * line -- the body of save_matrix (cols = C) and save_vector (cols = 1),
+ * fileio.py:94-101, :118-123, formatted on the device.  buf == NULL: size
+ * query. */
+int imp_format_values(const double* x, int64_t n, int64_t cols,
+                      int32_t device, char* buf, int64_t cap,
+                      int64_t* out_len);
+
 /* Cumulative kernel launches issued by the library: our own kernels and
  * CUB primitive calls (radix sort / scan), graph replays included. */
 void imp_launch_count(unsigned long long* mine, unsigned long long* cub);

@@ -25,7 +25,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
-UNITS = ["imdp.cu", "sweep.cu", "build.cu"]
+UNITS = ["imdp.cu", "sweep.cu", "build.cu", "export.cu"]
 JIT_SOURCES = ["ndtr.h", "jit/construct.cuh"]
 
 

@@ -14,7 +14,7 @@ import numpy as np
 from .errors import (AbstractionError, ConvergenceError, ImpactError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libimpact_b200.so")
+LIB_PATH = os.environ.get("IMP_LIB_PATH") or os.path.join(HERE, "libimpact_b200.so")
 
 IMP_OK, IMP_E_ARG, IMP_E_CUDA, IMP_E_ABSTRACTION, IMP_E_NONFINITE, \
     IMP_E_CONVERGENCE, IMP_E_MONOTONE, IMP_E_BRACKET, IMP_E_JIT, \
@@ -103,6 +103,10 @@ def _declare(lib):
     lib.imp_fp64_peak.argtypes = [c_i32, P_dbl]
     lib.imp_jit_compile.argtypes = [ctypes.POINTER(BuildDesc),
                                     ctypes.c_char_p]
+    lib.imp_export_text_rows.argtypes = [c_vp, c_i32, c_i64, c_i64,
+                                         ctypes.c_char_p, c_i64, P_i64]
+    lib.imp_format_values.argtypes = [P_dbl, c_i64, c_i64, c_i32,
+                                      ctypes.c_char_p, c_i64, P_i64]
     lib.imp_time_sweep.argtypes = [c_vp, c_i32, c_i32, c_i32, P_dbl]
     lib.imp_time_sweep.restype = c_i32
     lib.imp_launch_count.argtypes = [ctypes.POINTER(ctypes.c_ulonglong),
@@ -122,7 +126,8 @@ EXPORTED = ("imp_last_error", "imp_version", "imp_device_query",
             "imp_jit_compile",
             "imp_run_phase", "imp_bellman_step", "imp_row_values",
             "imp_shard_sweep", "imp_fp64_peak", "imp_time_sweep",
-            "imp_launch_count")
+            "imp_launch_count", "imp_export_text_rows",
+            "imp_format_values")
 
 
 def launch_count():

@@ -174,13 +174,9 @@ struct SweepArgs {
   // gets never depends on its shard or neighbours)
   const int* list;
   int64_t n_list;
-  // when set, the list length lives on the device (rows the streaming
-  // verify pass could not settle, appended during the same iteration)
-  const unsigned long long* n_list_dev;
-  unsigned long long* miss_cnt;   // streaming pass: miss counter of the class
-  int* miss_list;                 // streaming pass: miss rows of the class
-  int* hint;            // (2 * n_phase_rows) warm-start crossing columns
-  int verify_hint;      // search kernel: try the hint before searching
+  unsigned long long* miss_total;  // IMP_SWEEP_STATS: [rows off the hint,
+                                   //  rows needing the bucketed search]
+  int* hint;            // (2 * n_phase_rows) last sweep's crossing columns
   const int* perm0;     // columns by rank (hint publication)
   const int* perm1;
   double* out0;
@@ -218,28 +214,6 @@ __device__ __forceinline__ int64_t phase_row(const SweepArgs& a, int64_t t) {
   return (k * a.n_u + a.fixed[k]) * a.n_w + i;
 }
 
-// Team-wide deterministic sum of two values.  TEAM == 32: warp only.  Larger
-// teams: warp partials -> shared memory -> every warp re-reduces the same
-// partials with the same tree (identical result everywhere, one barrier).
-template <int TEAM>
-__device__ __forceinline__ double2 team_sum2(double x, double y,
-                                             double2* part, int& parity) {
-  x = warp_sum(x);
-  y = warp_sum(y);
-  if constexpr (TEAM == 32) {
-    return make_double2(x, y);
-  } else {
-    constexpr int NW = TEAM / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double2* buf = part + parity * NW;
-    parity ^= 1;
-    if (lane == 0) buf[warp] = make_double2(x, y);
-    __syncthreads();
-    double2 v = lane < NW ? buf[lane] : make_double2(0.0, 0.0);
-    return make_double2(warp_sum(v.x), warp_sum(v.y));
-  }
-}
-
 // A row's value from its team-reduced sums (both K5 kernels use exactly
 // this expression): lower mass + filled head below the crossing rank P +
 // the partial fill of slot P.
@@ -250,243 +224,61 @@ __device__ __forceinline__ double row_value(double lw, double f, double s,
   return lw + x;
 }
 
-// One row per team.  TEAM threads hold up to TEAM*EPT stored entries in
-// registers (missing entries padded with h = 0, rank = +inf, so every loop
-// is unguarded and the per-lane sums do not depend on EPT); the two
-// virtual slots (target, avoid) live in team thread 0.
-//
-// Warm start: `hint` keeps, per phase row and track, the column of last
-// sweep's crossing slot (-1: no crossing, -2: unknown).  Near convergence
-// the global order barely moves, so the column's new rank usually verifies
-// with one two-sided probe (k_sweep_stream, below); otherwise the binary
-// search here runs.  Either way the value is computed from C(<P*) with the
-// same per-lane order and team tree, so the result is independent of the
-// hint and of which kernel settled the row (bitwise).
-// i-th row of this launch's class list: phase row t, CSR row, start,
-// length; team-uniform.
-__device__ __forceinline__ void class_row(const SweepArgs& a, int64_t i,
-                                         int64_t& t, int64_t& row,
-                                         int64_t& beg, int& m) {
-  t = a.list[i];
-  row = phase_row(a, t);
-  beg = a.row_ptr[row];
-  m = (int)(a.row_ptr[row + 1] - beg);
+// ---------------------------------------------------------------------------
+// Exact crossing arithmetic.  Each head h = hi - lo in [0, 1] is rounded to
+// the 2^-88 grid, h~ = RN(h * 2^88) / 2^88 (error <= 2^-89 per slot), and
+// C(<q) = sum of h~ over the row's slots of rank < q is an exact integer
+// multiple of 2^-88.  Integer sums do not depend on summation order, so the
+// crossing P (largest q with C(<q) < slack) is one well-defined number
+// however it is found: a verify pass at last sweep's crossing, or a
+// bucketed search with shared-memory atomics.
+// h~ is held as h~ * 2^88 = A * 2^44 + B (A = RN(h * 2^44) >= 0, B the
+// signed remainder, |B| <= 2^43), obtained with two magic-number roundings
+// in FP64 (no integer shifting).  Partial sums of A and of B over <= 2^14
+// slots stay below 2^59 in magnitude: plain 64-bit adds, no carries.
+// ---------------------------------------------------------------------------
+
+typedef unsigned __int128 u128;
+constexpr int FIX_BITS = 88;
+
+struct Fix {
+  uint64_t a, b;   // b: two's-complement int64
+};
+
+__device__ __forceinline__ Fix to_fix(double h) {
+  const double M1 = 384.0;       // 1.5 * 2^8: on [256, 512) the ulp is 2^-44
+  const double M2 = 0x1.8p52;    // 1.5 * 2^52: ulp 1
+  const double t = __dadd_rn(h, M1);            // 384 + RN(h, 2^-44)
+  const double r = __dsub_rn(h, __dsub_rn(t, M1));  // exact, |r| <= 2^-45
+  const double t2 = __fma_rn(r, 0x1p88, M2);    // M2 + RN(r * 2^88)
+  return Fix{(uint64_t)(__double_as_longlong(t) - __double_as_longlong(M1)),
+             (uint64_t)(__double_as_longlong(t2) - __double_as_longlong(M2))};
 }
 
-// STAGED (CTA teams): the next row's col / lo / hi stream into a shared
-// memory stage with cp.async (LDGSTS) while the current row -- already in
-// registers -- is being priced, so HBM latency overlaps the reductions.
-template <int TEAM, int EPT, bool WIDE, bool STAGED = false>
-__global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
-                                  TEAM == 32 ? 2 : (TEAM < 512 ? 512 / TEAM : 1))
-    k_sweep(SweepArgs a) {
-  if (a.ctl && a.ctl->done) return;
-  __shared__ double2 part[2 * (TEAM > 32 ? TEAM / 32 : 1)];
-  extern __shared__ double stage[];   // STAGED: lo[CAP] hi[CAP] col[CAP]
-  constexpr int CAP = TEAM * EPT;
-  // warp teams: one private stage per warp (20 B per entry = 2.5 doubles)
-  double* my_stage = TEAM == 32 ? stage + (threadIdx.x >> 5) * (CAP * 5 / 2)
-                                : stage;
-  double* s_lo = my_stage;
-  double* s_hi = my_stage + CAP;
-  int* s_col = reinterpret_cast<int*>(my_stage + 2 * CAP);
-  auto team_sync = [] {
-    if constexpr (TEAM == 32) __syncwarp();
-    else __syncthreads();
-  };
-  int parity = 0;
-  const int tid = TEAM == 32 ? (threadIdx.x & 31) : threadIdx.x;
-  const int64_t team0 = TEAM == 32
-      ? (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)
-      : (int64_t)blockIdx.x;
-  const int64_t nteams = TEAM == 32
-      ? (int64_t)gridDim.x * (blockDim.x >> 5) : (int64_t)gridDim.x;
+__device__ __forceinline__ u128 fix_value(uint64_t a, uint64_t b) {
+  return (u128)(((__int128)a << 44) + (__int128)(int64_t)b);
+}
 
-  auto issue = [&](int64_t beg, int m) {
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int q = e * TEAM + tid;
-      if (q < m) {
-        __pipeline_memcpy_async(s_lo + q, a.lo + beg + q, 8);
-        __pipeline_memcpy_async(s_hi + q, a.hi + beg + q, 8);
-        __pipeline_memcpy_async(s_col + q, a.col + beg + q, 4);
-      }
-    }
-    __pipeline_commit();
-  };
-
-  const int64_t n_list = a.n_list_dev ? (int64_t)*a.n_list_dev : a.n_list;
-  int64_t row = 0, beg = 0, t = 0;
-  int m = 0;
-  int64_t i = team0;
-  if (i < n_list) class_row(a, i, t, row, beg, m);
-  if constexpr (STAGED) {
-    if (i < n_list) issue(beg, m);
-  }
-  while (i < n_list) {
-    double h[EPT];
-    RankReg<WIDE> rk[EPT];
-    double lw0 = 0.0, lw1 = 0.0;
-    int64_t row_n = 0, beg_n = 0, t_n = 0;
-    int m_n = 0;
-    const int64_t i_n = i + nteams;
-    if constexpr (STAGED) {
-      __pipeline_wait_prior(0);
-      team_sync();
-    }
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      h[e] = 0.0;
-      rk[e].none();
-      const int q = e * TEAM + tid;
-      if (q < m) {
-        int c;
-        double l, u;
-        if constexpr (STAGED) {
-          c = s_col[q];
-          l = s_lo[q];
-          u = s_hi[q];
-        } else {
-          c = __ldg(a.col + beg + q);
-          l = __ldg(a.lo + beg + q);
-          u = __ldg(a.hi + beg + q);
-        }
-        h[e] = u - l;
-        const double2 w = __ldg(a.colw + c);
-        lw0 = fma(l, w.x, lw0);
-        lw1 = fma(l, w.y, lw1);
-        rk[e].load(a, c);
-      }
-    }
-    if constexpr (STAGED) {
-      if (i_n < n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
-      team_sync();                           // stage consumed
-      if (i_n < n_list) issue(beg_n, m_n);
-    }
-    // virtual slots n_s (target) and n_s + 1 (avoid) on team thread 0
-    double hv[2] = {0.0, 0.0};
-    RankReg<WIDE> rv[2];
-    rv[0].none();
-    rv[1].none();
-    if (tid == 0) {
-      const double lr = a.r_min[row], la = a.a_min[row];
-      hv[0] = a.r_max[row] - lr;
-      hv[1] = a.a_max[row] - la;
-      const double2 wr = __ldg(a.colw + a.n_s), wa = __ldg(a.colw + a.n_s + 1);
-      lw0 = fma(la, wa.x, fma(lr, wr.x, lw0));
-      lw1 = fma(la, wa.y, fma(lr, wr.y, lw1));
-      rv[0].load(a, a.n_s);
-      rv[1].load(a, a.n_s + 1);
-    }
-    const double s = a.slack[row];
-
-    // C(<q) for both tracks: the one reduction every decision is based on
-    auto below = [&](int q0, int q1) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        if (rk[e].r0() < q0) s0 += h[e];
-        if (rk[e].r1() < q1) s1 += h[e];
-      }
-      if (tid == 0) {
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          if (rv[v].r0() < q0) s0 += hv[v];
-          if (rv[v].r1() < q1) s1 += hv[v];
-        }
-      }
-      return team_sum2<TEAM>(s0, s1, part, parity);
-    };
-
-    // warm start: rank of last sweep's crossing entry
-    int g0 = -2, g1 = -2;
-    if (a.hint && a.verify_hint) {
-      const int hq[2] = {a.hint[2 * t], a.hint[2 * t + 1]};
-      int gr[2];
-#pragma unroll
-      for (int o = 0; o < 2; ++o) {
-        gr[o] = hq[o];
-        if (hq[o] >= 0) {
-          RankReg<WIDE> r;
-          r.load(a, hq[o]);
-          gr[o] = o ? r.r1() : r.r0();
-        } else if (hq[o] == -1) {
-          gr[o] = a.n;          // "no crossing": verify C(<n) < s
-        }
-      }
-      g0 = gr[0];
-      g1 = gr[1];
-    }
-    int p0 = 0, p1 = 0;
-    double c0 = 0.0, c1 = 0.0;
-    // zero slack: nothing is filled, P = 0 with C = 0 (what the search gives)
-    bool ok0 = !(s > 0.0), ok1 = !(s > 0.0);
-    if (!ok0 && (g0 >= 0 || g1 >= 0)) {
-      const int a0 = g0 >= 0 ? g0 : 0, a1 = g1 >= 0 ? g1 : 0;
-      const double2 lt = below(a0, a1);
-      const double2 le = below(a0 + 1, a1 + 1);
-      ok0 = g0 >= 0 && lt.x < s && (g0 == a.n || le.x >= s);
-      ok1 = g1 >= 0 && lt.y < s && (g1 == a.n || le.y >= s);
-      if (ok0) { p0 = g0; c0 = lt.x; }
-      if (ok1) { p1 = g1; c1 = lt.y; }
-    }
-    if (!(ok0 && ok1)) {
-      // binary search for P (largest rank with C(<P) < slack)
-      int b0 = 0, b1 = 0;
-      double d0 = 0.0, d1 = 0.0;
-      for (int b = a.nbits - 1; b >= 0; --b) {
-        const int q0 = b0 + (1 << b), q1 = b1 + (1 << b);
-        const double2 tot = below(q0, q1);
-        if (q0 <= a.n && tot.x < s) { b0 = q0; d0 = tot.x; }
-        if (q1 <= a.n && tot.y < s) { b1 = q1; d1 = tot.y; }
-      }
-      if (!ok0) { p0 = b0; c0 = d0; }
-      if (!ok1) { p1 = b1; c1 = d1; }
-    }
-    // filled part: sum_{rank<P} head * w, weights regathered by rank
-    double f0 = 0.0, f1 = 0.0;
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const int r0 = rk[e].r0(), r1 = rk[e].r1();
-      if (r0 < p0) f0 = fma(h[e], __ldg(a.ws0 + r0), f0);
-      if (r1 < p1) f1 = fma(h[e], __ldg(a.ws1 + r1), f1);
-    }
-    if (tid == 0) {
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int r0 = rv[v].r0(), r1 = rv[v].r1();
-        if (r0 < p0) f0 = fma(hv[v], __ldg(a.ws0 + r0), f0);
-        if (r1 < p1) f1 = fma(hv[v], __ldg(a.ws1 + r1), f1);
-      }
-    }
-    const double2 lw = team_sum2<TEAM>(lw0, lw1, part, parity);
-    const double2 g = team_sum2<TEAM>(f0, f1, part, parity);
-    if (tid == 0) {
-      if (a.hint) {   // publish the crossing columns (ws index = rank)
-        a.hint[2 * t] = p0 >= a.n ? -1 : __ldg(a.perm0 + p0);
-        a.hint[2 * t + 1] = p1 >= a.n ? -1 : __ldg(a.perm1 + p1);
-      }
-      a.out0[t] = row_value(lw.x, g.x, s, c0, p0, a.n, a.ws0);
-      a.out1[t] = row_value(lw.y, g.y, s, c1, p1, a.n, a.ws1);
-    }
-    if constexpr (!STAGED) {
-      if (i_n < n_list) class_row(a, i_n, t_n, row_n, beg_n, m_n);
-    }
-    i = i_n;
-    t = t_n;
-    row = row_n;
-    beg = beg_n;
-    m = m_n;
-  }
+// ceil(s * 2^88): C < s  <=>  C * 2^88 < ceil(s * 2^88) for integer C * 2^88
+__device__ __forceinline__ u128 fix_ceil(double s) {
+  if (!(s > 0.0)) return 0;
+  const uint64_t u = (uint64_t)__double_as_longlong(s);
+  const int e = (int)((u >> 52) & 0x7ff);
+  if (e == 0) return 1;
+  const uint64_t M = (u & 0xfffffffffffffull) | (1ull << 52);
+  const int sh = e - 1075 + FIX_BITS;
+  if (sh >= 0) return (u128)M << sh;
+  const int k = -sh;
+  if (k >= 64) return 1;
+  return (u128)((M >> k) + ((M & ((1ull << k) - 1)) != 0));
 }
 
 
-// Team sum of K values with exactly team_sum2's tree per value (warp xor
-// butterfly; CTA teams: warp partials -> shared memory -> every warp
-// re-reduces the NW partials), so the streaming pass reproduces the search
-// kernel's sums bit for bit.
+// Team sums.  Floats: per value a warp xor butterfly, then (CTA teams) warp
+// partials through shared memory re-reduced by every warp -- a fixed tree,
+// so a row's sums depend only on its contents and TEAM.  Integers: exact.
 template <int TEAM, int K>
-__device__ __forceinline__ void team_sum_k(double* v, double* part) {
+__device__ __forceinline__ void team_sum_f(double* v, double* part) {
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
   if constexpr (TEAM > 32) {
@@ -500,116 +292,407 @@ __device__ __forceinline__ void team_sum_k(double* v, double* part) {
 #pragma unroll
     for (int k = 0; k < K; ++k)
       v[k] = warp_sum(lane < NW ? part[k * NW + lane] : 0.0);
-    __syncthreads();   // part is reused by the team's next row
+    __syncthreads();
   }
 }
 
-// K5a, streaming verify pass: one read of the row settles it when last
-// sweep's crossing column still marks the crossing in the new order.  Per
-// lane, in the search kernel's entry order (q = e * TEAM + tid), it
-// accumulates  sum l*w,  C(<g), C(<g+1) and  sum_{rank<g} h*w  for both
-// tracks (g = the hinted column's new rank); nothing is kept in registers
-// across entries, so the pass runs at low register count and high
-// occupancy.  Rows whose guess fails (or is unknown) are appended to the
-// class's miss list and priced by k_sweep (binary search) right after.
+// Pass-A team sums of 6 doubles (the fixed tree of team_sum_f) in one
+// exchange; CTA teams clear `clear` (the window buffer of the next row)
+// between the two barriers, where no teammate can still be reading it
+// (last row) or already writing it (next row).
+template <int TEAM>
+__device__ __forceinline__ void team_sum_pass_a(double* f, double* fpart,
+                                                double* clear, int n_clear) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) f[k] = warp_sum(f[k]);
+  if constexpr (TEAM > 32) {
+    constexpr int NW = TEAM / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) fpart[k * NW + warp] = f[k];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < n_clear; q += TEAM) clear[q] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      f[k] = warp_sum(lane < NW ? fpart[k * NW + lane] : 0.0);
+    __syncthreads();
+  } else {
+    __syncwarp();
+    for (int q = threadIdx.x & 31; q < n_clear; q += 32) clear[q] = 0.0;
+    __syncwarp();
+  }
+}
+
+// Certified float decisions.  The canonical float sum Cf of <= 2^14 + 2
+// heads (each in [0, 1]) is within m * 2^-53 * Cf of the true sum, which is
+// within 2^-75 of the exact fixed-point sum C~ -- so |Cf - C~| < margin(Cf)
+// and a comparison of Cf against s that clears the margin decides the exact
+// comparison the search would make.  Anything closer is left to the exact
+// search.  (Window walks add < 2^7 more float adds: the 2^-36 slope covers
+// them.)
+__device__ __forceinline__ double k5_margin(double c) {
+  return fma(fabs(c), 0x1p-36, 0x1p-68);
+}
+
+// Buckets per search level: CTA teams 256, warp teams 128.
+template <int TEAM>
+struct K5Shape {
+  static constexpr int NW = TEAM > 32 ? TEAM / 32 : 1;
+#ifndef IMP_K5_LOGB_WARP
+#define IMP_K5_LOGB_WARP 7
+#endif
+  static constexpr int LOGB = TEAM > 32 ? 8 : IMP_K5_LOGB_WARP;
+  static constexpr int B = 1 << LOGB;
+  // per team: float partials, integer partials, histogram [track][bucket]
+  // {a, b}, search broadcast
+  static constexpr int F_PART = 6 * NW;
+  static constexpr int HIST = 2 * B * 2;
+  // pass A captures h~ of the slots with rank in [g - W, g + W) per track,
+  // so a crossing that moved by < W ranks is resolved exactly in registers
+  // / shared memory without a search (only the float sum F needs a pass)
+  static constexpr int W = TEAM > 32 ? 32 : 8;
+  static constexpr int WIN = 2 * 2 * W;   // [track][slot] heads
+};
+
+// Stream the row's slots in the canonical per-lane order -- entries
+// q = tid, tid + TEAM, ... (U loads in flight), then the two virtual slots
+// on team thread 0 -- calling f(l, h, w, rank) for each.
+template <int TEAM, bool WIDE, class Fn>
+__device__ __forceinline__ void for_slots(const SweepArgs& a, int tid,
+                                          int64_t row, int64_t beg, int m,
+                                          Fn&& f) {
+#ifndef IMP_K5_U
+#define IMP_K5_U 4
+#endif
+  constexpr int U = IMP_K5_U;
+  const int32_t* colp = a.col + beg;
+  const double* lop = a.lo + beg;
+  const double* hip = a.hi + beg;
+  for (int q = tid; q < m; q += U * TEAM) {
+    int c[U];
+    double l[U], u[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int qq = q + k * TEAM;
+      c[k] = -1;
+      l[k] = u[k] = 0.0;
+      if (qq < m) {
+        c[k] = __ldg(colp + qq);
+        l[k] = __ldg(lop + qq);
+        u[k] = __ldg(hip + qq);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (c[k] >= 0) {
+        RankReg<WIDE> rk;
+        rk.load(a, c[k]);
+        f(l[k], u[k] - l[k], __ldg(a.colw + c[k]), rk);
+      }
+    }
+  }
+  if (tid == 0) {   // virtual slots n_s (target) and n_s + 1 (avoid)
+    const double lr = a.r_min[row], la = a.a_min[row];
+    const double hr = a.r_max[row] - lr, ha = a.a_max[row] - la;
+    RankReg<WIDE> rk;
+    rk.load(a, a.n_s);
+    f(lr, hr, __ldg(a.colw + a.n_s), rk);
+    rk.load(a, a.n_s + 1);
+    f(la, ha, __ldg(a.colw + a.n_s + 1), rk);
+  }
+}
+
+// Team-uniform state of the bucketed search (shared memory).
+struct SearchState {
+  u128 cb[2];      // exact C(< lo) of the current range
+  u128 C[2];       // result: C(<P)
+  int lo[2], lg[2];  // current rank range [lo, lo + 2^lg)
+  int P[2];        // result
+  int pick[2];     // bucket chosen by the scan (-1: none)
+  int act;         // bit o: track o still searching
+};
+
+// Levels of the exact search: each level is one pass over the row adding
+// every in-range slot's h~ into its rank bucket (shared-memory atomics:
+// exact, order-free), then one warp scans the buckets for the first whose
+// inclusive cumulative sum reaches s; the range shrinks to that bucket.
+// On return st.P / st.C hold P and C(<P) of every track searched.
+template <int TEAM, bool WIDE>
+__device__ __noinline__ void search_levels(const SweepArgs& a, int tid,
+                                           int64_t row, int64_t beg, int m,
+                                           double s, SearchState& st,
+                                           unsigned long long* hist) {
+  using SH = K5Shape<TEAM>;
+  auto team_sync = [] {
+    if constexpr (TEAM == 32) __syncwarp();
+    else __syncthreads();
+  };
+  const u128 S = fix_ceil(s);
+  while (st.act) {
+    const int act = st.act;
+    const int lo0 = st.lo[0], lo1 = st.lo[1];
+    const int w0 = (act & 1) ? 1 << st.lg[0] : 0;
+    const int w1 = (act & 2) ? 1 << st.lg[1] : 0;
+    const int sh0 = max(0, st.lg[0] - SH::LOGB), sh1 = max(0, st.lg[1] - SH::LOGB);
+    for (int q = tid; q < SH::HIST; q += TEAM) hist[q] = 0ull;
+    team_sync();
+    for_slots<TEAM, WIDE>(a, tid, row, beg, m,
+        [&](double, double h, double2, const RankReg<WIDE>& rk) {
+          const unsigned d0 = (unsigned)(rk.r0() - lo0);
+          const unsigned d1 = (unsigned)(rk.r1() - lo1);
+          const bool in0 = d0 < (unsigned)w0, in1 = d1 < (unsigned)w1;
+          if (!(in0 || in1)) return;
+          const Fix x = to_fix(h);
+          if (in0) {
+            unsigned long long* hb = hist + (d0 >> sh0) * 2;
+            atomicAdd(hb, (unsigned long long)x.a);
+            atomicAdd(hb + 1, (unsigned long long)x.b);
+          }
+          if (in1) {
+            unsigned long long* hb = hist + (SH::B + (d1 >> sh1)) * 2;
+            atomicAdd(hb, (unsigned long long)x.a);
+            atomicAdd(hb + 1, (unsigned long long)x.b);
+          }
+        });
+    team_sync();
+    if (tid < 32) {   // one warp scans each active track's buckets
+      const int lane = tid;
+      constexpr int PER = SH::B / 32;
+#pragma unroll 1
+      for (int o = 0; o < 2; ++o) {
+        if (!(act >> o & 1)) continue;
+        const unsigned long long* hb = hist + (o * SH::B + lane * PER) * 2;
+        u128 mine = 0;
+#pragma unroll 1
+        for (int k = 0; k < PER; ++k) mine += fix_value(hb[2 * k], hb[2 * k + 1]);
+        u128 inc = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint64_t ylo = __shfl_up_sync(FULL, (uint64_t)inc, d);
+          const uint64_t yhi = __shfl_up_sync(FULL, (uint64_t)(inc >> 64), d);
+          if (lane >= d) inc += ((u128)yhi << 64) | ylo;
+        }
+        const u128 cb = st.cb[o];
+        const unsigned hit = __ballot_sync(FULL, cb + inc >= S);
+        if (hit) {
+          const int L = __ffs(hit) - 1;
+          if (lane == L) {
+            u128 run = cb + inc - mine;
+            int pick = -1;
+#pragma unroll 1
+            for (int k = 0; k < PER && pick < 0; ++k) {
+              const u128 v = fix_value(hb[2 * k], hb[2 * k + 1]);
+              if (run + v >= S) pick = lane * PER + k;
+              else run += v;
+            }
+            const int sh = o ? sh1 : sh0;
+            st.cb[o] = run;
+            st.lo[o] += pick << sh;
+            st.lg[o] = sh;
+            if (sh == 0) {
+              st.P[o] = st.lo[o];
+              st.C[o] = run;
+              st.act &= ~(1 << o);
+            }
+          }
+        } else if (lane == 31) {
+          // the whole range stays below s -- only on the first level
+          // (total < s): no crossing, P = n, C(<n) = total
+          st.P[o] = a.n;
+          st.C[o] = cb + inc;
+          st.act &= ~(1 << o);
+        }
+        __syncwarp();
+      }
+    }
+    team_sync();
+  }
+}
+
+// K5: twin greedy-LP values of one class of phase rows, one row per team
+// (warp or CTA).  Value of a row for one track:
+//   val = sum l*w + [ sum_{rank<P} h*w + (s - C(<P)) * w_sorted[P] ]
+// with the float sums in the canonical per-lane order + fixed team tree,
+// and C / P exact (above).
+//   pass A   one read of the row: sum l*w, and at g = the rank of last
+//            sweep's crossing column: C(<g), C(<g+1), sum_{rank<g} h*w.
+//            C(<g) < s <= C(<g+1) proves P = g -> done (most rows).
+//   search   otherwise, per level one pass with a shared-memory histogram
+//            of exact head sums over B rank buckets of the current range;
+//            a warp scan picks the bucket where the cumulative sum reaches
+//            s; the range shrinks by B per level (2-4 levels), to one rank.
+//   pass F   sum_{rank<P} h*w for the searched tracks (same order/tree as A).
+// The result does not depend on the hint, on which path settled the row,
+// or on the row's position / shard: bitwise-identical rows give
+// bitwise-identical values.
+#ifndef IMP_K5_TPSM
+#define IMP_K5_TPSM 1024   // resident threads per SM the register cap targets
+#endif
 template <int TEAM, bool WIDE>
 __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
-                                  TEAM == 32 ? 4 : 1024 / TEAM)
-    k_sweep_stream(SweepArgs a) {
+                                  (TEAM == 32 ? 256 : TEAM) < IMP_K5_TPSM
+                                      ? IMP_K5_TPSM / (TEAM == 32 ? 256 : TEAM)
+                                      : 1)
+    k_sweep(SweepArgs a) {
   if (a.ctl && a.ctl->done) return;
-  constexpr int NW = TEAM > 32 ? TEAM / 32 : 1;
-  constexpr int U = 4;   // entries in flight per lane
-  __shared__ double part[8 * NW];
+  using SH = K5Shape<TEAM>;
+  constexpr int TEAMS_PER_BLOCK = TEAM == 32 ? 8 : 1;
+  __shared__ double f_part[SH::F_PART];
+  __shared__ unsigned long long hist_all[TEAMS_PER_BLOCK][SH::HIST];
+  __shared__ SearchState s_st[TEAMS_PER_BLOCK];
+  __shared__ double s_win[TEAMS_PER_BLOCK][2][SH::WIN];   // row parity
+  __shared__ double s_fv[TEAMS_PER_BLOCK][6];
   const int tid = TEAM == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  const int slot = TEAM == 32 ? (threadIdx.x >> 5) : 0;
+  unsigned long long* hist = hist_all[slot];
   const int64_t team0 = TEAM == 32
       ? (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)
       : (int64_t)blockIdx.x;
   const int64_t nteams = TEAM == 32
       ? (int64_t)gridDim.x * (blockDim.x >> 5) : (int64_t)gridDim.x;
+  auto team_sync = [] {
+    if constexpr (TEAM == 32) __syncwarp();
+    else __syncthreads();
+  };
+  for (int q = tid; q < 2 * SH::WIN; q += TEAM) (&s_win[slot][0][0])[q] = 0.0;
+  team_sync();
+
   for (int64_t i = team0; i < a.n_list; i += nteams) {
     const int64_t t = a.list[i];
     const int64_t row = phase_row(a, t);
     const int64_t beg = a.row_ptr[row];
     const int m = (int)(a.row_ptr[row + 1] - beg);
     const double s = a.slack[row];
-    const bool zero = !(s > 0.0);   // nothing filled: P = 0, C = 0
+    const bool zero = !(s > 0.0);   // nothing is filled: P = 0, C = 0
+    bool known = zero;
     int g0 = 0, g1 = 0;
-    if (!zero) {
+    if (!zero && a.hint) {
       const int h0 = a.hint[2 * t], h1 = a.hint[2 * t + 1];
-      if (h0 < -1 || h1 < -1) {     // unknown (first sweep): search
-        if (tid == 0) a.miss_list[atomicAdd(a.miss_cnt, 1ull)] = (int)t;
-        continue;
+      if (h0 >= -1 && h1 >= -1) {
+        known = true;
+        RankReg<WIDE> r;
+        if (h0 >= 0) { r.load(a, h0); g0 = r.r0(); } else g0 = a.n;
+        if (h1 >= 0) { r.load(a, h1); g1 = r.r1(); } else g1 = a.n;
       }
-      RankReg<WIDE> r;
-      if (h0 >= 0) { r.load(a, h0); g0 = r.r0(); } else g0 = a.n;
-      if (h1 >= 0) { r.load(a, h1); g1 = r.r1(); } else g1 = a.n;
     }
-    // v: lw0 lw1 | C(<g) 0 1 | C(<g+1) 0 1 | F(<g) 0 1
-    double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    const int32_t* colp = a.col + beg;
-    const double* lop = a.lo + beg;
-    const double* hip = a.hi + beg;
-    for (int q = tid; q < m; q += U * TEAM) {
-      int c[U];
-      double l[U], u[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int qq = q + k * TEAM;
-        c[k] = -1;
-        l[k] = u[k] = 0.0;
-        if (qq < m) {
-          c[k] = __ldcs(colp + qq);
-          l[k] = __ldcs(lop + qq);
-          u[k] = __ldcs(hip + qq);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if (c[k] >= 0) {
-          const double2 w = __ldg(a.colw + c[k]);
-          RankReg<WIDE> rk;
-          rk.load(a, c[k]);
-          const double h = u[k] - l[k];
-          v[0] = fma(l[k], w.x, v[0]);
-          v[1] = fma(l[k], w.y, v[1]);
+    // ---- pass A ----------------------------------------------------------
+    // fv: lw0 lw1 | F0 F1 (sum h*w, rank < g) | C0 C1 (sum h, rank < g),
+    // all float in the canonical order; heads ranked in [g - W, g + W) are
+    // captured per track.  The window buffer is double-buffered by row
+    // parity (cleared during the previous row's reduction).
+    constexpr int W = SH::W;
+    const int par = (int)((i / nteams) & 1);
+    double* win = s_win[slot][par];
+    const int wb0 = g0 - W, wb1 = g1 - W;
+    double fv[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for_slots<TEAM, WIDE>(a, tid, row, beg, m,
+        [&](double l, double h, double2 w, const RankReg<WIDE>& rk) {
+          fv[0] = fma(l, w.x, fv[0]);
+          fv[1] = fma(l, w.y, fv[1]);
           const int r0 = rk.r0(), r1 = rk.r1();
-          if (r0 < g0) { v[2] += h; v[6] = fma(h, w.x, v[6]); }
-          if (r1 < g1) { v[3] += h; v[7] = fma(h, w.y, v[7]); }
-          if (r0 <= g0) v[4] += h;
-          if (r1 <= g1) v[5] += h;
-        }
-      }
-    }
-    if (tid == 0) {   // virtual slots n_s (target) and n_s + 1 (avoid)
-      const double lr = a.r_min[row], la = a.a_min[row];
-      const double hv[2] = {a.r_max[row] - lr, a.a_max[row] - la};
-      const double2 wv[2] = {__ldg(a.colw + a.n_s), __ldg(a.colw + a.n_s + 1)};
-      v[0] = fma(la, wv[1].x, fma(lr, wv[0].x, v[0]));
-      v[1] = fma(la, wv[1].y, fma(lr, wv[0].y, v[1]));
+          if (r0 < g0) { fv[2] = fma(h, w.x, fv[2]); fv[4] += h; }
+          if (r1 < g1) { fv[3] = fma(h, w.y, fv[3]); fv[5] += h; }
+          const unsigned d0 = (unsigned)(r0 - wb0), d1 = (unsigned)(r1 - wb1);
+          if (d0 < 2 * W) win[d0] = h;
+          if (d1 < 2 * W) win[2 * W + d1] = h;
+        });
+    team_sum_pass_a<TEAM>(fv, f_part, s_win[slot][par ^ 1], SH::WIN);
+    int P[2] = {g0, g1};
+    // need: 0 settled at g, 1 settled in the window (F, C need a pass),
+    // 2 needs the exact bucketed search (+ that pass)
+    int need[2] = {0, 0};
+    if (!zero) {
 #pragma unroll
       for (int o = 0; o < 2; ++o) {
-        RankReg<WIDE> rk;
-        rk.load(a, a.n_s + o);
-        const int r0 = rk.r0(), r1 = rk.r1();
-        if (r0 < g0) { v[2] += hv[o]; v[6] = fma(hv[o], wv[o].x, v[6]); }
-        if (r1 < g1) { v[3] += hv[o]; v[7] = fma(hv[o], wv[o].y, v[7]); }
-        if (r0 <= g0) v[4] += hv[o];
-        if (r1 <= g1) v[5] += hv[o];
+        if (!known) { need[o] = 2; continue; }
+        const int g = P[o];
+        const double* wt = win + o * 2 * W;
+        double c = fv[4 + o];
+        if (c + k5_margin(c) < s) {
+          if (g >= a.n) continue;                              // P = n
+          c += wt[W];
+          if (c - k5_margin(c) >= s) continue;                 // P = g
+          if (!(c + k5_margin(c) < s)) { need[o] = 2; continue; }
+          int q = g + 1;                                       // walk up
+          need[o] = 2;
+          for (; q < g + W; ++q) {
+            if (q >= a.n) { P[o] = a.n; need[o] = 1; break; }
+            const double cn = c + wt[q - g + W];
+            if (cn - k5_margin(cn) >= s) { P[o] = q; need[o] = 1; break; }
+            if (!(cn + k5_margin(cn) < s)) break;              // too close
+            c = cn;
+          }
+        } else if (c - k5_margin(c) >= s) {
+          const double mg = k5_margin(c);   // errors of the larger sums
+          int q = g - 1;                                       // walk down
+          need[o] = 2;
+          for (; q >= g - W && q >= 0; --q) {
+            c -= wt[q - g + W];
+            if (c + mg < s) { P[o] = q; need[o] = 1; break; }
+            if (!(c - mg >= s)) break;                         // too close
+          }
+        } else {
+          need[o] = 2;
+        }
       }
     }
-    team_sum_k<TEAM, 8>(v, part);
-    const bool ok0 = zero || (v[2] < s && (g0 >= a.n || v[4] >= s));
-    const bool ok1 = zero || (v[3] < s && (g1 >= a.n || v[5] >= s));
-    if (tid == 0) {
-      if (ok0 && ok1) {
-        a.out0[t] = row_value(v[0], v[6], s, v[2], g0, a.n, a.ws0);
-        a.out1[t] = row_value(v[1], v[7], s, v[3], g1, a.n, a.ws1);
-      } else {
-        a.miss_list[atomicAdd(a.miss_cnt, 1ull)] = (int)t;
+    // ---- bucketed exact search for unsettled tracks ----------------------
+    // Team-uniform search state lives in shared memory (st), so the pass-A
+    // registers are free during the search.
+    if (need[0] | need[1]) {
+      SearchState& st = s_st[slot];
+      if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s_fv[slot][k] = fv[k];
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          st.lo[o] = 0;
+          st.lg[o] = a.nbits;
+          st.cb[o] = 0;
+          st.P[o] = P[o];
+        }
+        st.act = (need[0] == 2 ? 1 : 0) | (need[1] == 2 ? 2 : 0);
+        if (a.miss_total) atomicAdd(a.miss_total + (st.act ? 1 : 0), 1ull);
       }
+      team_sync();
+      if (need[0] == 2 || need[1] == 2)
+        search_levels<TEAM, WIDE>(a, tid, row, beg, m, s, st, hist);
+      // ---- pass F: the canonical float sums below the new crossings -----
+      // (same per-lane order and team tree as pass A, so a row's bits do not
+      // depend on which path found P)
+      const int q0 = need[0] ? st.P[0] : -1, q1 = need[1] ? st.P[1] : -1;
+      double fz[4] = {0.0, 0.0, 0.0, 0.0};
+      for_slots<TEAM, WIDE>(a, tid, row, beg, m,
+          [&](double, double h, double2 w, const RankReg<WIDE>& rk) {
+            if (rk.r0() < q0) { fz[0] = fma(h, w.x, fz[0]); fz[2] += h; }
+            if (rk.r1() < q1) { fz[1] = fma(h, w.y, fz[1]); fz[3] += h; }
+          });
+      team_sum_f<TEAM, 4>(fz, f_part);
+#pragma unroll
+      for (int k = 0; k < 6; ++k) fv[k] = s_fv[slot][k];
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        if (need[o]) {
+          fv[2 + o] = fz[o];
+          fv[4 + o] = fz[2 + o];
+        }
+        P[o] = st.P[o];
+      }
+      team_sync();   // st is reused by the team's next row
+    }
+    if (tid == 0) {
+      if (a.hint && (need[0] | need[1])) {   // crossing columns for next sweep
+        a.hint[2 * t] = P[0] >= a.n ? -1 : __ldg(a.perm0 + P[0]);
+        a.hint[2 * t + 1] = P[1] >= a.n ? -1 : __ldg(a.perm1 + P[1]);
+      }
+      a.out0[t] = row_value(fv[0], fv[2], s, fv[4], P[0], a.n, a.ws0);
+      a.out1[t] = row_value(fv[1], fv[3], s, fv[5], P[1], a.n, a.ws1);
     }
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // Robust Bellman reduction + convergence statistics
@@ -818,9 +901,7 @@ struct Work {
   static constexpr int NCLASS = 8;
   DevBuf<int> class_rows;
   DevBuf<unsigned long long> class_cnt;   // counts, then scatter cursors
-  DevBuf<int> miss_rows;                  // K5a misses, class-partitioned
-  DevBuf<unsigned long long> miss_cnt;    // per class
-  DevBuf<unsigned long long> miss_total;  // IMP_SWEEP_STATS: misses, sweeps
+  DevBuf<unsigned long long> miss_total;  // IMP_SWEEP_STATS: rows searched
   int64_t class_off[NCLASS + 1] = {};
   bool classes_all = false;   // class lists hold the unfixed phase
 
@@ -844,8 +925,6 @@ struct Work {
     IMP_CUDA(cudaMemset(hint.ptr, 0xfe, hint.bytes()));   // -2: unknown
     class_rows.alloc(std::max<int64_t>(phase_rows, 1));
     class_cnt.alloc(2 * NCLASS);
-    miss_rows.alloc(std::max<int64_t>(phase_rows, 1));
-    miss_cnt.alloc(NCLASS);
     miss_total.alloc(2);
     IMP_CUDA(cudaMemset(miss_total.ptr, 0, miss_total.bytes()));
     colw.alloc(n);
@@ -940,13 +1019,8 @@ void build_classes(const imp_imdp* h, Work& w, const int64_t* fixed_dev,
   count_launches(phase_rows > 0 ? 2 : 0, 0);
 }
 
-struct Team {
-  int team, ept;
-};
-
-// IMP_SWEEP_STATS=1: per-iteration K5a miss counts accumulate on the
-// device (one extra tiny launch per iteration) and imp_run_phase prints
-// the miss rate to stderr.
+// IMP_SWEEP_STATS=1: the number of rows that needed the bucketed search
+// accumulates on the device and imp_run_phase prints the rate to stderr.
 bool sweep_stats() {
   static const int on = [] {
     const char* e = getenv("IMP_SWEEP_STATS");
@@ -955,62 +1029,9 @@ bool sweep_stats() {
   return on != 0;
 }
 
-__global__ void k_miss_accum(const Ctl* ctl, const unsigned long long* cnt,
-                             int nclass, unsigned long long* total) {
-  if (ctl && ctl->done) return;
-  unsigned long long m = 0;
-  for (int c = 0; c < nclass; ++c) m += cnt[c];
-  total[0] += m;
-  total[1] += 1;
-}
-
-// IMP_SWEEP_STREAM=0 disables K5a (search kernel only), for A/B timing.
-bool stream_disabled() {
-  static const int off = [] {
-    const char* e = getenv("IMP_SWEEP_STREAM");
-    return e && e[0] == '0' ? 1 : 0;
-  }();
-  return off != 0;
-}
-
-Team choose_team(int max_row) {
-  const int need = std::max(max_row, 1);
-  for (int e : {1, 2, 4, 8, 16})
-    if (need <= 32 * e) return {32, e};
-  for (int t : {64, 128, 256, 512, 1024})
-    if (need <= t * 16) return {t, 16};
-  return {0, 0};
-}
-
-template <int TEAM, int EPT, bool WIDE>
-void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
-  // CTA teams stage the next row through shared memory when one row of
-  // col/lo/hi (20 B per entry) fits
-  // (warp teams: one stage per warp, 8 warps per block)
-  constexpr int PER_BLOCK = TEAM == 32 ? 8 : 1;
-  constexpr bool STAGED = TEAM * EPT * 20 * PER_BLOCK <= 200 * 1024 &&
-                          (TEAM > 32 || EPT >= 4);
-  auto kern = k_sweep<TEAM, EPT, WIDE, STAGED>;
-  const size_t smem = STAGED ? (size_t)TEAM * EPT * 20 * PER_BLOCK : 0;
-  if (smem > 48 * 1024)
-    IMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-  int threads = TEAM == 32 ? 256 : TEAM;
-  int per_sm = 0;
-  IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
-                                                         threads, smem));
-  per_sm = std::max(per_sm, 1);
-  int64_t teams_per_block = TEAM == 32 ? threads / 32 : 1;
-  int64_t need = (a.n_list + teams_per_block - 1) / teams_per_block;
-  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * per_sm));
-  kern<<<blocks, threads, smem, s>>>(a);
-  IMP_CUDA(cudaGetLastError());
-}
-
-
 template <int TEAM, bool WIDE>
-void launch_stream_t(const SweepArgs& a, int sms, cudaStream_t s) {
-  auto kern = k_sweep_stream<TEAM, WIDE>;
+void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
+  auto kern = k_sweep<TEAM, WIDE>;
   const int threads = TEAM == 32 ? 256 : TEAM;
   int per_sm = 0;
   IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
@@ -1025,95 +1046,33 @@ void launch_stream_t(const SweepArgs& a, int sms, cudaStream_t s) {
 }
 
 template <bool WIDE>
-void launch_stream_w(const SweepArgs& a, int team, int sms, cudaStream_t s) {
+void launch_sweep_w(const SweepArgs& a, int team, int sms, cudaStream_t s) {
   switch (team) {
-    case 32: return launch_stream_t<32, WIDE>(a, sms, s);
-    case 64: return launch_stream_t<64, WIDE>(a, sms, s);
-    case 128: return launch_stream_t<128, WIDE>(a, sms, s);
-    case 256: return launch_stream_t<256, WIDE>(a, sms, s);
-    default: return launch_stream_t<512, WIDE>(a, sms, s);
+    case 32: return launch_sweep_t<32, WIDE>(a, sms, s);
+    case 128: return launch_sweep_t<128, WIDE>(a, sms, s);
+    case 256: return launch_sweep_t<256, WIDE>(a, sms, s);
+    default: return launch_sweep_t<512, WIDE>(a, sms, s);
   }
 }
 
-template <bool WIDE>
-void launch_sweep_w(const SweepArgs& a, Team tm, int sms, cudaStream_t s) {
-  switch (tm.team) {
-    case 32:
-      switch (tm.ept) {
-        case 1: return launch_sweep_t<32, 1, WIDE>(a, sms, s);
-        case 2: return launch_sweep_t<32, 2, WIDE>(a, sms, s);
-        case 4: return launch_sweep_t<32, 4, WIDE>(a, sms, s);
-        case 8: return launch_sweep_t<32, 8, WIDE>(a, sms, s);
-        case 12: return launch_sweep_t<32, 12, WIDE>(a, sms, s);
-        default: return launch_sweep_t<32, 16, WIDE>(a, sms, s);
-      }
-    case 64: return launch_sweep_t<64, 16, WIDE>(a, sms, s);
-    case 128: return launch_sweep_t<128, 16, WIDE>(a, sms, s);
-    case 256: return launch_sweep_t<256, 16, WIDE>(a, sms, s);
-    default:
-      if (tm.ept == 32) return launch_sweep_t<512, 32, WIDE>(a, sms, s);
-      return launch_sweep_t<512, 16, WIDE>(a, sms, s);
-  }
-}
-
-// K5 over all phase rows: one launch per non-empty row class (classes are
-// fixed functions of a row's stored length m -- see kClassHi -- so the
-// kernel and summation tree a row gets never depend on the shard):
-//   warp team   m <= 128 / 256 / 384 / 512 (EPT 4 / 8 / 12 / 16; padding
-//               adds +0.0 and does not change any sum)
-//   CTA teams   m <= 2048 / 4096 / 8192 / 16384 (128 / 256 / 512 / 512x32)
+// K5 over all phase rows: one launch per non-empty row class.  Classes are
+// fixed functions of a row's stored length m (kClassHi), so the team -- and
+// with it every float summation tree -- a row gets never depends on its
+// shard: warp teams for m <= 512, CTAs of 128 / 256 / 512 threads above.
 // Returns the number of launches.
-//
-// With warm-start hints (phase loops), every class first runs the
-// streaming verify pass K5a (k_sweep_stream), which settles the rows whose
-// crossing column carried over from the last sweep and appends the rest to
-// the class's miss list; then the search kernel K5b (k_sweep) prices the
-// misses, with the list length read on the device (graph-capturable, no
-// host sync).  Both kernels produce identical bits for a row.
 int launch_sweep(SweepArgs sa, const Work& w, bool wide, int sms,
                  cudaStream_t s) {
   static const int teams[] = {32, 32, 32, 32, 128, 256, 512, 512};
-  static const int epts[] = {4, 8, 12, 16, 16, 16, 16, 32};
   int launches = 0;
-  const bool two_pass = sa.hint != nullptr && !stream_disabled();
-  if (two_pass) {
-    IMP_CUDA(cudaMemsetAsync(w.miss_cnt.ptr, 0, w.miss_cnt.bytes(), s));
-    for (int c = 0; c < Work::NCLASS; ++c) {
-      const int64_t cnt = w.class_off[c + 1] - w.class_off[c];
-      if (cnt == 0) continue;
-      SweepArgs a = sa;
-      a.list = w.class_rows.ptr + w.class_off[c];
-      a.n_list = cnt;
-      a.miss_cnt = w.miss_cnt.ptr + c;
-      a.miss_list = w.miss_rows.ptr + w.class_off[c];
-      if (wide) launch_stream_w<true>(a, teams[c], sms, s);
-      else launch_stream_w<false>(a, teams[c], sms, s);
-      ++launches;
-    }
-  }
+  if (sa.hint && sweep_stats()) sa.miss_total = w.miss_total.ptr;
   for (int c = 0; c < Work::NCLASS; ++c) {
     const int64_t cnt = w.class_off[c + 1] - w.class_off[c];
     if (cnt == 0) continue;
     SweepArgs a = sa;
-    if (two_pass) {
-      a.list = w.miss_rows.ptr + w.class_off[c];
-      a.n_list = cnt;                        // grid bound; true count below
-      a.n_list_dev = w.miss_cnt.ptr + c;
-      a.verify_hint = 0;                     // K5a already tried it
-    } else {
-      a.list = w.class_rows.ptr + w.class_off[c];
-      a.n_list = cnt;
-      a.verify_hint = sa.hint != nullptr;
-    }
-    Team tm{teams[c], epts[c]};
-    if (wide) launch_sweep_w<true>(a, tm, sms, s);
-    else launch_sweep_w<false>(a, tm, sms, s);
-    ++launches;
-  }
-  if (two_pass && sweep_stats()) {
-    k_miss_accum<<<1, 1, 0, s>>>(sa.ctl, w.miss_cnt.ptr, Work::NCLASS,
-                                 w.miss_total.ptr);
-    IMP_CUDA(cudaGetLastError());
+    a.list = w.class_rows.ptr + w.class_off[c];
+    a.n_list = cnt;
+    if (wide) launch_sweep_w<true>(a, teams[c], sms, s);
+    else launch_sweep_w<false>(a, teams[c], sms, s);
     ++launches;
   }
   return launches;
@@ -1340,14 +1299,15 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     cudaEventDestroy(e1);
 
     if (sweep_stats()) {
-      unsigned long long mt[2];
+      unsigned long long mt[2] = {0, 0};
       IMP_CUDA(cudaMemcpy(mt, w.miss_total.ptr, sizeof(mt),
                           cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[imp] phase: %lld iterations, %lld rows, K5a misses "
-              "%llu of %llu row sweeps (%.2f%%), %.3f ms/iteration\n",
-              hc.it, (long long)phase_rows, mt[0],
-              mt[1] * (unsigned long long)phase_rows,
-              mt[1] ? 100.0 * mt[0] / (double)(mt[1] * phase_rows) : 0.0,
+      const double sweeps = (double)hc.it * (double)phase_rows;
+      fprintf(stderr, "[imp] phase: %lld iterations, %lld rows: crossing "
+              "moved in %.2f%% of row sweeps, bucketed search in %.2f%%; "
+              "%.3f ms/iteration\n", hc.it, (long long)phase_rows,
+              sweeps > 0 ? 100.0 * mt[0] / sweeps : 0.0,
+              sweeps > 0 ? 100.0 * mt[1] / sweeps : 0.0,
               hc.it ? ms / hc.it : 0.0);
     }
     const int cur = hc.cur;
