@@ -52,6 +52,23 @@ def _peaks():
         return {}
 
 
+def _ncu_traffic(config):
+    """DRAM bytes per algorithmic unit from the committed ncu --set full
+    captures (profiles/*/ncu_traffic.json, dram__bytes_read.sum +
+    dram__bytes_write.sum of one launch / its units), newest round first."""
+    base = os.path.join(ROOT, "profiles")
+    try:
+        rounds = sorted(os.listdir(base), reverse=True)
+    except OSError:
+        return None
+    for r in rounds:
+        path = os.path.join(base, r, "ncu_traffic.json")
+        if os.path.exists(path):
+            with open(path) as fh:
+                return json.load(fh).get(config)
+    return None
+
+
 # --- clocks sampling during the timed region -------------------------------
 
 class ClockSampler:
@@ -314,12 +331,25 @@ def run_b200(args):
         "peak_source": "measured DFMA microbenchmark (imp_fp64_peak), "
                        "2 flops/DFMA",
     }
+    # the same bytes over the whole in-loop iteration (order keys, sorts,
+    # ranks, K5 incl. moved-crossing passes, Bellman, control)
+    loop_gbs = sweep_bytes * sweeps_per_s / 1e9
+    traffic = _ncu_traffic(args.config)
     roofline_sweep = {
         "kernel": "k_sweep", "bound": "hbm", "achieved": sweep_gbs,
         "peak": hbm, "unit": "GB/s", "frac": sweep_gbs / hbm,
-        "traffic": None, "bytes_per_sweep": sweep_bytes,
+        "traffic": (traffic["k_sweep_bytes_per_entry"] * nnz
+                    if traffic and "k_sweep_bytes_per_entry" in traffic
+                    else None),
+        "bytes_per_sweep": sweep_bytes,
         "kernel_ms": ms_sweep.value, "peak_source": hbm_note,
+        "in_loop": {"gbs": loop_gbs, "frac": loop_gbs / hbm,
+                    "note": "phase-1 iterations of the timed steps: same "
+                            "algorithmic bytes over the full iteration time"},
     }
+    if traffic and "k_refine_dram_bytes_per_eval" in traffic:
+        roofline["traffic"] = traffic["k_refine_dram_bytes_per_eval"] * \
+            report.nm_evals
 
     cpu = None
     if not args.no_cpu_baseline:

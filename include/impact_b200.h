@@ -237,6 +237,35 @@ int imp_time_sweep(imp_imdp* h, int32_t spec, int32_t lp, int32_t reps,
                    double* ms);
 
 /* ---------------------------------------------------------------------- */
+/* Closed-loop simulation (cli.py:163-251, cmd_simulate)                   */
+/* ---------------------------------------------------------------------- */
+
+typedef struct imp_sim_desc {
+  int32_t rollouts, steps;
+  uint64_t seed;             /* [synthesis] seed (derive_seed(seed, r, 0))  */
+  int32_t reach_like;        /* spec reach / reach-avoid                     */
+  int32_t n_starts;
+  const int32_t* starts;     /* (n_starts) controller slots                  */
+  int32_t n_ctrl;
+  const double* coords;      /* (n_ctrl, n) controller state coordinates     */
+  const int32_t* slot_input; /* (n_ctrl) input index of each slot's policy   */
+  int64_t total;             /* state lattice size                           */
+  const int32_t* slot_of;    /* (total) controller slot of a flat state, -1  */
+  const uint8_t* kind;       /* (total) 1 avoid, 2 target, 0 other           */
+  const double* lb;          /* (n) state space                              */
+  const double* ub;
+  /* desc->consts here: (n_u, n_consts) folded at (u_j, disturbance centre) */
+} imp_sim_desc;
+
+/* All rollouts at once, one GPU thread each, bit-identical to the
+ * reference's loop for dynamics without x-dependent library calls.
+ * trace: (rollouts, steps + 1, n) visited points (the first length[r] rows
+ * of each rollout are valid); satisfied: (rollouts) 0/1.  A non-finite
+ * dynamics value -> IMP_E_NONFINITE (EvalError). */
+int imp_simulate(const imp_build_desc* d, const imp_sim_desc* s,
+                 double* trace, int32_t* length, int32_t* satisfied);
+
+/* ---------------------------------------------------------------------- */
 /* Text export in the reference's file formats (fileio.py)                 */
 /* ---------------------------------------------------------------------- */
 

@@ -26,17 +26,23 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
 UNITS = ["imdp.cu", "sweep.cu", "build.cu", "export.cu"]
-JIT_SOURCES = ["ndtr.h", "jit/construct.cuh"]
+JIT_SOURCES = {"kJitPrelude": ["ndtr.h", "ziggurat_tables.h", "rng.h"],
+               "kJitKernels": ["jit/construct.cuh", "jit/simulate.cuh"]}
 
 
 def _embed_jit():
     """Write csrc/_jit_source.inc: the JIT sources as C++ raw strings
-    (kJitPrelude = ndtr.h, kJitKernels = jit/construct.cuh); the generated
-    config + dynamics go between them at run time."""
+    (kJitPrelude = ndtr.h + numpy's random streams, kJitKernels = the
+    construction and simulation kernels); the generated config + dynamics
+    go between them at run time."""
     decls = []
-    for name, rel in zip(("kJitPrelude", "kJitKernels"), JIT_SOURCES):
-        with open(os.path.join(CSRC, rel)) as fh:
-            body = fh.read().replace("#pragma once", "")
+    for name, rels in JIT_SOURCES.items():
+        body = ""
+        for rel in rels:
+            with open(os.path.join(CSRC, rel)) as fh:
+                text = fh.read().replace("#pragma once", "")
+            body += "\n".join(line for line in text.split("\n")
+                              if not line.startswith('#include "')) + "\n"
         chunks = [body[i:i + 12000] for i in range(0, len(body), 12000)]
         lit = "\n".join(f'R"IMPJIT({c})IMPJIT"' for c in chunks)
         decls.append(f"static const char {name}[] =\n{lit};\n")

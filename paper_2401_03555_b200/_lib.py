@@ -66,6 +66,15 @@ class PhaseDesc(ctypes.Structure):
                 ("max_iterations", c_i64), ("fixed_policy", P_i64)]
 
 
+class SimDesc(ctypes.Structure):
+    _fields_ = [("rollouts", c_i32), ("steps", c_i32),
+                ("seed", ctypes.c_uint64), ("reach_like", c_i32),
+                ("n_starts", c_i32), ("starts", P_i32), ("n_ctrl", c_i32),
+                ("coords", P_dbl), ("slot_input", P_i32), ("total", c_i64),
+                ("slot_of", P_i32), ("kind", ctypes.POINTER(ctypes.c_uint8)),
+                ("lb", P_dbl), ("ub", P_dbl)]
+
+
 class PhaseOut(ctypes.Structure):
     _fields_ = [("v0", P_dbl), ("v1", P_dbl), ("policy", P_i64),
                 ("iterations", c_i64), ("k0", c_i64), ("k1", c_i64),
@@ -107,6 +116,9 @@ def _declare(lib):
                                          ctypes.c_char_p, c_i64, P_i64]
     lib.imp_format_values.argtypes = [P_dbl, c_i64, c_i64, c_i32,
                                       ctypes.c_char_p, c_i64, P_i64]
+    lib.imp_simulate.argtypes = [ctypes.POINTER(BuildDesc),
+                                 ctypes.POINTER(SimDesc), P_dbl, P_i32,
+                                 P_i32]
     lib.imp_time_sweep.argtypes = [c_vp, c_i32, c_i32, c_i32, P_dbl]
     lib.imp_time_sweep.restype = c_i32
     lib.imp_launch_count.argtypes = [ctypes.POINTER(ctypes.c_ulonglong),
@@ -127,7 +139,7 @@ EXPORTED = ("imp_last_error", "imp_version", "imp_device_query",
             "imp_run_phase", "imp_bellman_step", "imp_row_values",
             "imp_shard_sweep", "imp_fp64_peak", "imp_time_sweep",
             "imp_launch_count", "imp_export_text_rows",
-            "imp_format_values")
+            "imp_format_values", "imp_simulate")
 
 
 def launch_count():

@@ -83,7 +83,7 @@ struct BuildParams {
 struct JitModule {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t mean = nullptr, outer = nullptr, refine = nullptr,
-               assemble = nullptr;
+               assemble = nullptr, simulate = nullptr;
 };
 
 std::mutex g_jit_mu;
@@ -193,6 +193,7 @@ JitModule& jit(int device, const std::string& config, const std::string& dyn) {
   IMP_CUDA(cudaLibraryGetKernel(&m.outer, m.lib, "k_outer"));
   IMP_CUDA(cudaLibraryGetKernel(&m.refine, m.lib, "k_refine"));
   IMP_CUDA(cudaLibraryGetKernel(&m.assemble, m.lib, "k_assemble"));
+  IMP_CUDA(cudaLibraryGetKernel(&m.simulate, m.lib, "k_simulate"));
   return g_jit_cache.emplace(key, m).first->second;
 }
 
@@ -526,6 +527,110 @@ extern "C" int imp_jit_compile(const imp_build_desc* d, const char* cubin_path) 
       IMP_REQUIRE(f, "cannot open %s", cubin_path);
       fwrite(cubin.data(), 1, cubin.size(), f);
       fclose(f);
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Closed-loop simulation (cli.py:177-251): k_simulate of the JIT module
+// ---------------------------------------------------------------------------
+
+namespace imp {
+namespace {
+// Mirror of the JIT module's SimParams (jit/simulate.cuh); same layout.
+struct SimParamsHost {
+  int rollouts, steps, n_starts, reach_like;
+  unsigned long long seed;
+  const int* starts;
+  const double* coords;
+  const int* slot_of;
+  const unsigned char* kind;
+  const int* slot_input;
+  const double* consts;
+  const double* lb;
+  const double* ub;
+  const double* eta;
+  const int* counts;
+  const double* sigma;
+  double* trace;
+  int* length;
+  int* satisfied;
+  unsigned long long* err;
+};
+}  // namespace
+}  // namespace imp
+
+extern "C" int imp_simulate(const imp_build_desc* d, const imp_sim_desc* sd,
+                            double* trace, int32_t* length,
+                            int32_t* satisfied) {
+  return guarded([&] {
+    IMP_REQUIRE(d && sd && trace && length && satisfied, "null argument");
+    IMP_REQUIRE(d->n >= 1 && d->n <= 16, "state dimension unsupported");
+    IMP_REQUIRE(sd->rollouts >= 1 && sd->steps >= 1,
+                "rollouts and steps must be >= 1");
+    IMP_REQUIRE(sd->n_starts >= 1 && sd->n_ctrl >= 1, "empty controller");
+    IMP_REQUIRE(d->dyn_source, "missing dynamics source");
+    const int N = d->n;
+    IMP_CUDA(cudaSetDevice(d->device));
+    JitModule& M = jit(d->device, config_header(d), d->dyn_source);
+    cudaStream_t s;
+    IMP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
+    const int64_t npts = (int64_t)sd->rollouts * (sd->steps + 1) * N;
+    auto starts = upload(sd->starts, sd->n_starts, s);
+    auto coords = upload(sd->coords, (size_t)sd->n_ctrl * N, s);
+    auto slot_of = upload(sd->slot_of, sd->total, s);
+    auto kind = upload(sd->kind, sd->total, s);
+    auto slot_input = upload(sd->slot_input, sd->n_ctrl, s);
+    auto consts = upload(d->consts, (size_t)d->n_u * std::max(d->n_consts, 1), s);
+    auto lb = upload(sd->lb, N, s);
+    auto ub = upload(sd->ub, N, s);
+    auto eta = upload(d->eta, N, s);
+    auto counts = upload(d->counts, N, s);
+    auto sigma = upload(d->sigma, N, s);
+    DevBuf<double> tr(npts);
+    DevBuf<int> len(sd->rollouts), sat(sd->rollouts);
+    DevBuf<unsigned long long> err(1);
+    IMP_CUDA(cudaMemsetAsync(err.ptr, 0xff, sizeof(unsigned long long), s));
+    SimParamsHost P{};
+    P.rollouts = sd->rollouts;
+    P.steps = sd->steps;
+    P.n_starts = sd->n_starts;
+    P.reach_like = sd->reach_like;
+    P.seed = sd->seed;
+    P.starts = starts.ptr;
+    P.coords = coords.ptr;
+    P.slot_of = slot_of.ptr;
+    P.kind = kind.ptr;
+    P.slot_input = slot_input.ptr;
+    P.consts = consts.ptr;
+    P.lb = lb.ptr;
+    P.ub = ub.ptr;
+    P.eta = eta.ptr;
+    P.counts = counts.ptr;
+    P.sigma = sigma.ptr;
+    P.trace = tr.ptr;
+    P.length = len.ptr;
+    P.satisfied = sat.ptr;
+    P.err = err.ptr;
+    void* args[] = {&P};
+    const unsigned block = 128;
+    IMP_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(M.simulate),
+                              dim3((sd->rollouts + block - 1) / block),
+                              dim3(block), args, 0, s));
+    count_launches(1, 0);
+    unsigned long long e = 0;
+    IMP_CUDA(cudaMemcpyAsync(&e, err.ptr, sizeof(e), cudaMemcpyDeviceToHost, s));
+    IMP_CUDA(cudaMemcpyAsync(trace, tr.ptr, sizeof(double) * npts,
+                             cudaMemcpyDeviceToHost, s));
+    IMP_CUDA(cudaMemcpyAsync(length, len.ptr, sizeof(int) * sd->rollouts,
+                             cudaMemcpyDeviceToHost, s));
+    IMP_CUDA(cudaMemcpyAsync(satisfied, sat.ptr, sizeof(int) * sd->rollouts,
+                             cudaMemcpyDeviceToHost, s));
+    IMP_CUDA(cudaStreamSynchronize(s));
+    if (e != ~0ull) {
+      set_error("domain error evaluating the dynamics (rollout %llu)", e);
+      throw Failure{IMP_E_NONFINITE};
     }
   });
 }
