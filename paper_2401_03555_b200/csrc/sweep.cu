@@ -352,7 +352,10 @@ struct K5Shape {
   // pass A captures h~ of the slots with rank in [g - W, g + W) per track,
   // so a crossing that moved by < W ranks is resolved exactly in registers
   // / shared memory without a search (only the float sum F needs a pass)
-  static constexpr int W = TEAM > 32 ? 32 : 8;
+#ifndef IMP_K5_WWARP
+#define IMP_K5_WWARP 8
+#endif
+  static constexpr int W = TEAM > 32 ? 32 : IMP_K5_WWARP;
   static constexpr int WIN = 2 * 2 * W;   // [track][slot] heads
 };
 
