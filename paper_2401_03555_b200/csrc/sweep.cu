@@ -336,12 +336,12 @@ __device__ __forceinline__ double k5_margin(double c) {
   return fma(fabs(c), 0x1p-36, 0x1p-68);
 }
 
-// Buckets per search level: CTA teams 256, warp teams 128.
+// Buckets per search level: CTA teams 256, warp teams 32.
 template <int TEAM>
 struct K5Shape {
   static constexpr int NW = TEAM > 32 ? TEAM / 32 : 1;
 #ifndef IMP_K5_LOGB_WARP
-#define IMP_K5_LOGB_WARP 7
+#define IMP_K5_LOGB_WARP 5
 #endif
   static constexpr int LOGB = TEAM > 32 ? 8 : IMP_K5_LOGB_WARP;
   static constexpr int B = 1 << LOGB;
@@ -353,7 +353,7 @@ struct K5Shape {
   // so a crossing that moved by < W ranks is resolved exactly in registers
   // / shared memory without a search (only the float sum F needs a pass)
 #ifndef IMP_K5_WWARP
-#define IMP_K5_WWARP 8
+#define IMP_K5_WWARP 32
 #endif
   static constexpr int W = TEAM > 32 ? 32 : IMP_K5_WWARP;
   static constexpr int WIN = 2 * 2 * W;   // [track][slot] heads
