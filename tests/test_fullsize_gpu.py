@@ -92,7 +92,7 @@ def test_robot2d_reachavoid_shards_bitwise(ra):
 
 def test_dim14_scalar_recursion():
     """dim14 (16 384 states, every row identical up to symmetry): after k
-    phase-1 sweeps V0 = a_max (1 - (1 - a_max)^k) exactly as the scalar
+    phase-1 sweeps V0_k = 1 - (1 - a)^k: the scalar
     recursion V' = a + (1 - a) V of the max-LP (SURVEY.md finding 7)."""
     cfg = benchmark("dim14_verify")
     im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
