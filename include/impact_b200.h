@@ -136,6 +136,15 @@ typedef struct imp_build_desc {
   int32_t multistart;        /* 0 -> 1 + 2*dim                              */
   /* shard: safe states [k_begin, k_begin + k_count) */
   int32_t k_begin, k_count;
+  /* Monte Carlo noise (FullNormal, noise.py:41-73, 133-153): mc = 1 runs
+   * the reference's _row_monte_carlo (abstraction.py:511-540) -- every
+   * destination, NM over the MC cell probability of mc_samples samples
+   * from Generator(Philox(SeedSequence(derive_seed(mc_seed, row, dest)))) */
+  int32_t mc;
+  int32_t mc_samples;
+  uint64_t mc_seed;
+  double mc_norm;            /* sqrt(det(inv_cov)) * (2 pi)^(-n/2), numpy  */
+  const double* inv_cov;     /* (n, n)                                      */
 } imp_build_desc;
 
 /* Per-build timings (device milliseconds, CUDA events) and counters. */

@@ -49,7 +49,10 @@ class BuildDesc(ctypes.Structure):
                 ("consts", P_dbl), ("deps", P_i32), ("n_deps", P_i32),
                 ("zero_cutoff", c_dbl), ("tol", c_dbl), ("low_cost", c_i32),
                 ("max_evals_per_dim", c_i32), ("multistart", c_i32),
-                ("k_begin", c_i32), ("k_count", c_i32)]
+                ("k_begin", c_i32), ("k_count", c_i32),
+                ("mc", c_i32), ("mc_samples", c_i32),
+                ("mc_seed", ctypes.c_uint64), ("mc_norm", c_dbl),
+                ("inv_cov", P_dbl)]
 
 
 class BuildStats(ctypes.Structure):

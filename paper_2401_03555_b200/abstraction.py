@@ -14,6 +14,7 @@ tests do, is uploaded on first use.
 """
 
 import ctypes
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -22,7 +23,7 @@ from . import _lib
 from .errors import AbstractionError
 from .expr import lower_dynamics
 from .grid import LabeledStates, Space, domain_box, multi_indices
-from .noise import DiagonalNormal
+from .noise import DiagonalNormal, FullNormal
 
 __all__ = ["AbstractionOptions", "RowIndex", "Imdp", "estimate_cost",
            "build_abstraction", "BuildReport"]
@@ -298,10 +299,11 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
         raise AbstractionError("input space dimension mismatch")
     if p and (dist is None or dist.dim != p):
         raise AbstractionError("disturbance space dimension mismatch")
-    if not isinstance(noise, DiagonalNormal):
+    monte_carlo = not isinstance(noise, DiagonalNormal)
+    if monte_carlo and not isinstance(noise, FullNormal):
         raise AbstractionError(
-            "only diagonal Gaussian noise runs on the B200 path (Monte "
-            "Carlo noise models are a later row, SURVEY.md 8(f))")
+            "custom-density noise does not run on the B200 path yet "
+            "(diagonal and full-covariance normal noise do)")
     if noise.dim != n:
         raise AbstractionError("noise dimension mismatch")
     n_s = len(labels.safe)
@@ -326,9 +328,11 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
     for d, dl in enumerate(lowered.deps):
         deps[d, :len(dl)] = dl
         n_deps[d] = len(dl)
+    sigma = np.ones(n) if monte_carlo else noise.sigma
+    inv_cov = _lib.as_f64(noise.inv_cov if monte_carlo else np.eye(n))
     arrays = dict(
         counts=counts, eta=_lib.as_f64(state.eta),
-        sigma=_lib.as_f64(noise.sigma), edges=edges,
+        sigma=_lib.as_f64(sigma), inv_cov=inv_cov, edges=edges,
         cover_lo=_lib.as_f64(cover.lo), cover_hi=_lib.as_f64(cover.hi),
         safe_multi=_lib.as_i32(safe_multi),
         target_multi=_lib.as_i32(multi_indices(state, labels.target)
@@ -341,7 +345,16 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
     desc.device = device
     desc.n, desc.m, desc.p = n, m, p
     desc.n_u, desc.n_w = n_u, n_w
-    desc.separable = int(dyn.is_separable())
+    desc.separable = int(dyn.is_separable()) and not monte_carlo
+    if monte_carlo:
+        # noise.py:63-73 (FullNormal.density), :133-153; abstraction.py:
+        # 378-397 (seeded per row and destination from mc_seed)
+        desc.mc = 1
+        desc.mc_samples = int(noise.samples)
+        desc.mc_seed = int(opts.mc_seed) & (2**64 - 1)
+        desc.mc_norm = (math.sqrt(np.linalg.det(noise.inv_cov))
+                        * (2 * math.pi) ** (-n / 2))
+    desc.inv_cov = _lib.ptr(arrays["inv_cov"], _lib.c_dbl)
     for key in ("counts", "safe_multi", "target_multi", "avoid_multi",
                 "deps", "n_deps"):
         setattr(desc, key, _lib.ptr(arrays[key], _lib.c_i32))

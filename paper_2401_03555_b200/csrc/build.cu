@@ -75,6 +75,11 @@ struct BuildParams {
   double* err_val;
   double sig[16];
   double sig_rcp[16];
+  long long row0;
+  int mc_samples;
+  unsigned long long mc_seed;
+  double mc_norm;
+  const double* inv_cov;
 };
 
 // JIT modules go through the runtime's library API (cudaLibrary_t /
@@ -110,6 +115,7 @@ std::string config_header(const imp_build_desc* d) {
   std::ostringstream o;
   o << "#define IMP_N " << d->n << "\n#define IMP_NC "
     << std::max(d->n_consts, 1) << "\n";
+  o << "#define IMP_MC " << (d->mc ? 1 : 0) << "\n";
   o << "#define IMP_MEAN_BLOCK " << nm_block(d->n) << "\n";
   o << "#define IMP_REFINE_BLOCK " << nm_block(d->n) << "\n";
   // tuning knobs (environment overrides for experiments)
@@ -383,18 +389,42 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     P.err = err.ptr;
     P.err_val = err_val.ptr;
 
+    // Monte Carlo noise: every destination of every row is an NM item
+    P.row0 = (long long)d->k_begin * d->n_u * d->n_w;
+    P.mc_samples = d->mc_samples;
+    P.mc_seed = d->mc_seed;
+    P.mc_norm = d->mc_norm;
+    DevBuf<double> g_inv;
+    if (d->mc) {
+      IMP_REQUIRE(d->inv_cov && d->mc_samples >= 2, "bad Monte Carlo noise");
+      g_inv = upload(d->inv_cov, (size_t)N * N, s);
+      P.inv_cov = g_inv.ptr;
+    }
+
+    // IMPACT_SYNC_STAGES=1: synchronize after every stage (fault isolation)
+    const bool sync_stages = getenv("IMPACT_SYNC_STAGES") != nullptr;
+    auto stage_done = [&](const char* name) {
+      if (!sync_stages) return;
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        set_error("stage %s: %s", name, cudaGetErrorString(e));
+        throw Failure{IMP_E_CUDA};
+      }
+    };
+
     // --- stage 1: mean ranges -------------------------------------------------
     // per-thread shared memory of the NM kernels (jit/construct.cuh:
     // imp_nm_doubles; k_refine adds its Instance record)
     const size_t nm_doubles = (size_t)(N + 4) * N + (N + 1);
-    const size_t inst_bytes = 5 * 8 + 5 * 4 + 4 + 2 * N * 8;
+    const size_t inst_bytes = 5 * 8 + 5 * 4 + 4 + 2 * N * 8 + (d->mc ? 8 : 0);
     const int block1 = nm_block(N);
-    if (n_rows > 0) {
+    if (n_rows > 0 && !d->mc) {
       const long long ntask = n_rows * N * 2;
       unsigned grid = (unsigned)std::min<long long>((ntask + block1 - 1) / block1,
                                                     (long long)sms * 64);
       launch(M.mean, grid, block1, block1 * nm_doubles * 8, s, P);
     }
+    stage_done("mean_ranges");
     IMP_CUDA(cudaEventRecord(ev.e[1], s));
 
     // --- stage 2: count, scan, write ---------------------------------------
@@ -405,6 +435,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
         1, std::min<long long>(n_rows, (long long)sms * 32));
     P.write = 0;
     if (n_rows > 0) launch(M.outer, grid2, 128, smem2, s, P);
+    stage_done("outer count");
     exclusive_scan(tcnt.ptr, reinterpret_cast<long long*>(row_ptr.ptr), n_rows + 1, s);
     exclusive_scan(xcnt.ptr, aux_ptr.ptr, n_rows + 1, s);
     long long nnz = 0, naux = 0;
@@ -428,11 +459,12 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     P.aux_max = aux_max.ptr;
     P.write = 1;
     if (n_rows > 0) launch(M.outer, grid2, 128, smem2, s, P);
+    stage_done("outer write");
     IMP_CUDA(cudaEventRecord(ev.e[2], s));
 
     // --- stage 3: NM refinement of the live window (coupled) ---------------
     long long instances = 0;
-    if (!d->separable && n_rows > 0) {
+    if ((!d->separable || d->mc) && n_rows > 0) {
       P.n_items = nnz + naux + n_rows;
       instances = 2 * P.n_items;
       const int block3 = nm_block(N);
@@ -450,6 +482,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
       const unsigned grid3 = (unsigned)std::max<long long>(
           1, std::min<long long>(need, (long long)sms * per_sm));
       launch(M.refine, grid3, block3, smem3, s, P);
+      stage_done("refine");
     }
     IMP_CUDA(cudaEventRecord(ev.e[3], s));
 

@@ -100,6 +100,12 @@ struct BuildParams {
   // and RN(1/sigma) for imp_div_rcp (NaN when sigma is outside 2^+-100)
   double sig[16];
   double sig_rcp[16];
+  // Monte Carlo noise (IMP_MC modules)
+  long long row0;             // global index of local row 0 (seeding)
+  int mc_samples;
+  unsigned long long mc_seed;
+  double mc_norm;
+  const double* inv_cov;      // (N, N)
 };
 
 __device__ __forceinline__ int imp_max_evals(const BuildParams& P, int dim) {
@@ -458,8 +464,10 @@ extern "C" __global__ void k_outer(BuildParams P) {
       s_mh[threadIdx.x] = P.mhi[r * IMP_N + threadIdx.x];
     }
     __syncthreads();
-    // exact per-dimension extremes (abstraction.py:287-297)
-    {
+    // exact per-dimension extremes (abstraction.py:287-297); Monte Carlo
+    // rows have no closed form: every destination is an NM item
+    // (abstraction.py:511-540)
+    if (!IMP_MC) {
       int d = 0, base = 0;
       for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
         while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
@@ -483,7 +491,12 @@ extern "C" __global__ void k_outer(BuildParams P) {
     // pruned box: a lattice point can only pass the cutoff if every factor
     // exceeds cutoff / prod_{e != d} max gmax_e (factors are <= 1); the
     // superlevel sets of the unimodal gmax_d are index intervals.
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && IMP_MC) {
+      for (int d = 0; d < IMP_N; ++d) {
+        s_blo[d] = 0;
+        s_bext[d] = P.counts[d];
+      }
+    } else if (threadIdx.x == 0) {
       double pm[IMP_N];
       int base = 0;
       for (int d = 0; d < IMP_N; ++d) {
@@ -538,7 +551,7 @@ extern "C" __global__ void k_outer(BuildParams P) {
             tmin = d == 0 ? c : tmin * c;
             base += P.counts[d];
           }
-          live = tmax > P.cutoff;
+          live = IMP_MC ? 1 : tmax > P.cutoff;
         }
       }
       int tot;
@@ -577,7 +590,7 @@ extern "C" __global__ void k_outer(BuildParams P) {
             tmin = d == 0 ? c : tmin * c;
             base += P.counts[d];
           }
-          live = tmax > P.cutoff;
+          live = IMP_MC ? 1 : tmax > P.cutoff;
           if (kind == 0) { rs[0] += tmin; rs[1] += tmax; }
           else { as[0] += tmin; as[1] += tmax; }
         }
@@ -639,8 +652,12 @@ struct Instance {
   int sgn;
   int kind;                    // 0: t entry, 1: aux (target/avoid), 2: cover
   double blo[IMP_N], bhi[IMP_N];
+#if IMP_MC
+  unsigned long long seed;     // derive_seed(mc_seed, row, destination)
+#endif
 };
-static_assert(sizeof(Instance) == 64 + 16 * IMP_N, "build.cu inst_bytes");
+static_assert(sizeof(Instance) == 64 + 16 * IMP_N + 8 * IMP_MC,
+              "build.cu inst_bytes");
 
 __device__ void imp_load_row(const BuildParams& P, Instance& I) {
   const long long r = I.row;
@@ -668,6 +685,15 @@ __device__ void imp_load_item(const BuildParams& P, Instance& I) {
     I.kind = 2;
     I.slot = I.row;
   }
+#if IMP_MC
+  {   // noise.py:121-125 derive_seed(mc_seed, row, dest), dest = flat state
+      // index (cover: the lattice size, abstraction.py:538-539)
+    const unsigned long long key[2] = {
+        (unsigned long long)(P.row0 + I.row),
+        (unsigned long long)(flat >= 0 ? flat : P.total)};
+    imp_seedseq(P.mc_seed, key, 2, &I.seed, 1);
+  }
+#endif
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) {
     double lo = P.cover_lo[d], hi = P.cover_hi[d];
@@ -752,6 +778,116 @@ __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
   return I.sgn ? prob * -1.0 : prob;
 }
 
+#if IMP_MC
+// Monte Carlo cell probability (noise.py:133-153 mc_box_probability with
+// FullNormal.density, :63-73): volume * mean(density(lo + (hi - lo) * U))
+// over mc_samples rows of U from the instance's Philox stream, the mean in
+// numpy's pairwise summation order (np.mean = add.reduce / n), generated
+// on the fly in stream order.  exp is glibc's (numpy's SIMD exp differs by
+// an ulp on ~5% of arguments), so values agree to ulps, not bits.
+struct ImpMc {
+  ImpPhilox g;
+  const BuildParams* P;
+  double lo[IMP_N], w[IMP_N], mean[IMP_N];
+  bool bad;
+};
+
+__device__ __forceinline__ double imp_mc_density(ImpMc& c) {
+  double diff[IMP_N];
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) {
+    const double y = c.lo[d] + c.w[d] * imp_philox_double(&c.g);
+    diff[d] = y - c.mean[d];
+  }
+  double q = 0.0;   // einsum("ki,ij,kj->k", diff, inv_cov, diff)
+#pragma unroll
+  for (int i = 0; i < IMP_N; ++i)
+#pragma unroll
+    for (int j = 0; j < IMP_N; ++j)
+      q += diff[i] * c.P->inv_cov[i * IMP_N + j] * diff[j];
+  const double v = c.P->mc_norm * imp_exp(-0.5 * q);
+  if (!imp_finite(v)) c.bad = true;
+  return v;
+}
+
+// numpy pairwise_sum of the next n densities (PW_BLOCKSIZE 128, 8 lanes):
+// leaves of <= 128 values summed as numpy does, split n -> (n2, n - n2) with
+// n2 = n/2 rounded down to a multiple of 8, combined left + right.  The
+// recursion runs on an explicit stack in stream order (no device
+// recursion, so the stack frame is static).
+__device__ double imp_mc_leaf(ImpMc& c, long long n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (long long i = 0; i < n; ++i) r += imp_mc_density(c);
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = imp_mc_density(c);
+  long long i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] += imp_mc_density(c);
+  }
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += imp_mc_density(c);
+  return res;
+}
+
+__device__ double imp_mc_pairwise(ImpMc& c, long long n) {
+  long long right[24];   // pending right halves (-1: right in progress)
+  double left[24];
+  int sp = 0;
+  long long cur = n;
+  for (;;) {
+    while (cur > 128) {
+      long long n2 = cur / 2;
+      n2 -= n2 % 8;
+      right[sp] = cur - n2;
+      ++sp;
+      cur = n2;
+    }
+    double val = imp_mc_leaf(c, cur);
+    for (;;) {
+      if (sp == 0) return val;
+      if (right[sp - 1] >= 0) {       // left subtree done: descend right
+        left[sp - 1] = val;
+        cur = right[sp - 1];
+        right[sp - 1] = -1;
+        break;
+      }
+      val = left[sp - 1] + val;       // right subtree done: combine
+      --sp;
+    }
+  }
+}
+
+__device__ double imp_mc_objective(const BuildParams& P, const Instance& I,
+                                   const double* x) {
+  double vol = 1.0;
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) vol = d == 0 ? I.bhi[0] - I.blo[0]
+                                               : vol * (I.bhi[d] - I.blo[d]);
+  double est = 0.0;
+  if (vol != 0.0) {
+    ImpMc c;
+    c.P = &P;
+    c.bad = false;
+    imp_f_all(x, I.K, c.mean);
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d) {
+      c.lo[d] = I.blo[d];
+      c.w[d] = I.bhi[d] - I.blo[d];
+    }
+    imp_philox_seed(&c.g, I.seed);
+    est = vol * (imp_mc_pairwise(c, P.mc_samples) / (double)P.mc_samples);
+    if (c.bad) est = IMP_INF - IMP_INF;   // NaN: flagged by the caller
+    else est = est > 0.0 ? (est < 1.0 ? est : 1.0) : 0.0;  // min(max(e,0),1)
+  }
+  return I.sgn ? est * -1.0 : est;
+}
+#endif
+
 __device__ void imp_store_instance(const BuildParams& P, const Instance& I,
                                    double best) {
   const double v = I.sgn ? -best : best;
@@ -821,7 +957,11 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
     if (live) {
       double p[IMP_N];
       nm.point(p);
+#if IMP_MC
+      double val = imp_mc_objective(P, I, p);
+#else
       double val = imp_box_objective(P, I, p, ndtr_tab);
+#endif
       if (!imp_finite(val)) {
         imp_flag_nonfinite(P, I.row);
         val = 0.0;
@@ -889,8 +1029,13 @@ extern "C" __global__ void k_assemble(BuildParams P) {
       for (long long q = xb + lane; q < xe; q += 32) {
         const int code = P.aux_code[q];
         const int off = code >= 0 ? 0 : 2;
-        s[off] += P.aux_min[q];
-        s[off + 1] += P.aux_max[q];
+        double mn = P.aux_min[q], mx = P.aux_max[q];
+        if (IMP_MC) {   // abstraction.py:518-522: cutoff, then min(pmin, pmax)
+          if (mx <= P.cutoff) mn = mx = 0.0;
+          mn = fmin(mn, mx);
+        }
+        s[off] += mn;
+        s[off + 1] += mx;
       }
       rmin = imp_warp_sum(s[0]);
       rmax = imp_warp_sum(s[1]);
@@ -900,8 +1045,13 @@ extern "C" __global__ void k_assemble(BuildParams P) {
     // clip t entries, t_min = min(t_min, t_max), low-cost zeroing
     double smin = 0.0, smax = 0.0;
     for (long long q = b + lane; q < e; q += 32) {
-      double hi = imp_clip(P.hi[q], 0.0, 1.0);
-      double lo = imp_clip(P.lo[q], 0.0, 1.0);
+      double hv = P.hi[q], lv = P.lo[q];
+      if (IMP_MC) {     // abstraction.py:518-522
+        if (hv <= P.cutoff) lv = hv = 0.0;
+        lv = fmin(lv, hv);
+      }
+      double hi = imp_clip(hv, 0.0, 1.0);
+      double lo = imp_clip(lv, 0.0, 1.0);
       if (P.low_cost && hi <= P.cutoff) lo = 0.0;
       lo = fmin(lo, hi);
       P.lo[q] = lo;

@@ -1,0 +1,83 @@
+"""Monte Carlo (full-covariance) noise path.
+
+Pinning chain: the reference's Monte Carlo abstraction of a small
+full-covariance system (tests/golden/mc_mc2d_full.npz, made by
+make_mc_golden.py) -> the oracle restatement (oracle/montecarlo.py, numpy's
+own random streams, einsum, exp and pairwise mean: bitwise) -> the GPU
+(k_refine with the Monte Carlo objective; numpy's streams restated in
+csrc/rng.h, glibc exp instead of numpy's SIMD exp, so values agree to a
+few ulps: observed <= 6e-17, tolerance 1e-12).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import iterate as OI
+from oracle import montecarlo as OM
+from paper_2401_03555_b200 import parse_config_text
+
+from . import golden_io as G
+
+TOL = 1e-12
+KEYS = ("t_min", "t_max", "r_min", "r_max", "a_min", "a_max")
+
+
+def fixture():
+    g = dict(np.load(os.path.join(G.GOLDEN, "mc_mc2d_full.npz")))
+    return g, parse_config_text(str(g["config"]))
+
+
+def test_oracle_rows_bitwise_vs_reference():
+    g, cfg = fixture()
+    rows = [0, 9, 27]
+    out = OM.build(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
+                   cfg.abstraction_options(), rows=rows)
+    for k in KEYS:
+        assert np.array_equal(out[k], g[k][rows]), k
+
+
+@pytest.mark.gpu
+def test_gpu_monte_carlo_abstraction_matches_reference():
+    from paper_2401_03555_b200 import build_abstraction
+    g, cfg = fixture()
+    im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
+                           cfg.abstraction_options())
+    for k in KEYS:
+        assert np.max(np.abs(getattr(im, k) - g[k])) <= TOL, k
+    # live sets: exact (no reference value sits within 1e-12 of the cutoff)
+    assert np.array_equal(im.t_max > 1e-12, g["t_max"] > 1e-12)
+
+
+@pytest.mark.gpu
+def test_gpu_monte_carlo_synthesis_matches_oracle():
+    from paper_2401_03555_b200 import build_abstraction, synthesize_reach
+    g, cfg = fixture()
+    im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
+                           cfg.abstraction_options())
+    c = synthesize_reach(im, eps=1e-6)
+    m = OI.Model(im.n_s, im.n_u, im.n_w, g["t_min"], g["t_max"], g["r_min"],
+                 g["r_max"], g["a_min"], g["a_max"])
+    want = OI.synthesize(m, "reach", eps=1e-6)
+    assert tuple(c.meta["iterations"]) == tuple(want["iterations"])
+    assert np.max(np.abs(c.p_min - want["p_min"])) <= 1e-9
+    assert np.max(np.abs(c.p_max - want["p_max"])) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_gpu_monte_carlo_large_sample_pairwise_tree():
+    """1000 samples: the pairwise mean splits into blocks (n > 128), the
+    Philox stream spans many blocks; rows against the oracle."""
+    from paper_2401_03555_b200 import build_abstraction
+    from paper_2401_03555_b200.noise import FullNormal
+    g, cfg = fixture()
+    noise = FullNormal(inv_cov=cfg.noise.inv_cov, det=cfg.noise.det,
+                       samples=1000)
+    im = build_abstraction(cfg.dynamics, noise, cfg.spaces, cfg.labels(),
+                           cfg.abstraction_options())
+    rows = [3, 20]
+    want = OM.build(cfg.dynamics, noise, cfg.spaces, cfg.labels(),
+                    cfg.abstraction_options(), rows=rows)
+    for k in ("t_min", "t_max"):
+        assert np.max(np.abs(getattr(im, k)[rows] - want[k])) <= TOL, k
