@@ -3,8 +3,8 @@
 Restates pkg/src/impact/abstraction.py's Monte Carlo path for FullNormal
 noise: _row_monte_carlo (:511-540) over every destination, _mc_prob_extremes
 (:378-397) through optimize_over_cell (optimize.py:165-189), and
-mc_box_probability / FullNormal.density / derive_seed / mc_generator
-(noise.py:63-73, 121-153) with numpy itself (the reference's dependency), so
+mc_box_probability / FullNormal.density / CustomNoise.density /
+derive_seed / mc_generator (noise.py:63-95, 121-153) with numpy itself (the reference's dependency), so
 its bits equal the reference's; pinned to tests/golden/mc_*.npz.
 """
 
@@ -22,19 +22,30 @@ def derive_seed(base, row, dest):
     return int(ss.generate_state(1, np.uint64)[0])
 
 
-def box_probability(inv_cov, samples, mean, lo, hi, seed):
-    """mc_box_probability(...)[0] with FullNormal.density."""
+def density(noise, y, mean):
+    """FullNormal.density (noise.py:63-73) / CustomNoise.density (:84-95)."""
+    if hasattr(noise, "inv_cov"):
+        diff = y - mean
+        quad = np.einsum("ki,ij,kj->k", diff, noise.inv_cov, diff)
+        n = noise.inv_cov.shape[0]
+        norm = math.sqrt(np.linalg.det(noise.inv_cov)) * \
+            (2 * math.pi) ** (-n / 2)
+        return norm * np.exp(-0.5 * quad)
+    env = {f"y{d + 1}": y[:, d] for d in range(noise.dim)}
+    env.update({f"m{d + 1}": mean[d] for d in range(noise.dim)})
+    return np.broadcast_to(np.asarray(
+        noise.density_expr.evaluate_env(env), dtype=float), (len(y),))
+
+
+def box_probability(noise, mean, lo, hi, seed):
+    """mc_box_probability(...)[0] (noise.py:133-153)."""
     volume = float(np.prod(hi - lo))
     if volume == 0.0:
         return 0.0
     rng = np.random.Generator(np.random.Philox(
         np.random.SeedSequence(entropy=int(seed) & (2**64 - 1))))
-    y = lo + (hi - lo) * rng.random((samples, len(lo)))
-    diff = y - mean
-    quad = np.einsum("ki,ij,kj->k", diff, inv_cov, diff)
-    n = inv_cov.shape[0]
-    norm = math.sqrt(np.linalg.det(inv_cov)) * (2 * math.pi) ** (-n / 2)
-    dens = norm * np.exp(-0.5 * quad)
+    y = lo + (hi - lo) * rng.random((noise.samples, len(lo)))
+    dens = density(noise, y, mean)
     est = volume * float(np.mean(dens))
     return min(max(est, 0.0), 1.0)
 
@@ -53,8 +64,8 @@ def extremes(ctx, noise, mc_seed, lo, hi, base, blo, bhi, row, dest):
                 env.update({f"x{d + 1}": p[d] for d in range(n)})
                 mean = np.array([float(e.evaluate(env))
                                  for e in ctx.dyn.exprs])
-                vals.append(sign * box_probability(
-                    noise.inv_cov, noise.samples, mean, blo, bhi, seed))
+                vals.append(sign * box_probability(noise, mean, blo, bhi,
+                                                   seed))
             return np.array(vals)
         best = minimize_batch(fn, lo, hi, start_points(lo, hi, ms),
                               ctx.max_evals(n), ctx.tol)

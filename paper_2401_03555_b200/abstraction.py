@@ -21,9 +21,9 @@ import numpy as np
 
 from . import _lib
 from .errors import AbstractionError
-from .expr import lower_dynamics
+from .expr import lower_density, lower_dynamics
 from .grid import LabeledStates, Space, domain_box, multi_indices
-from .noise import DiagonalNormal, FullNormal
+from .noise import CustomNoise, DiagonalNormal, FullNormal
 
 __all__ = ["AbstractionOptions", "RowIndex", "Imdp", "estimate_cost",
            "build_abstraction", "BuildReport"]
@@ -300,10 +300,9 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
     if p and (dist is None or dist.dim != p):
         raise AbstractionError("disturbance space dimension mismatch")
     monte_carlo = not isinstance(noise, DiagonalNormal)
-    if monte_carlo and not isinstance(noise, FullNormal):
-        raise AbstractionError(
-            "custom-density noise does not run on the B200 path yet "
-            "(diagonal and full-covariance normal noise do)")
+    custom = isinstance(noise, CustomNoise)
+    if monte_carlo and not (custom or isinstance(noise, FullNormal)):
+        raise AbstractionError("unsupported noise model")
     if noise.dim != n:
         raise AbstractionError("noise dimension mismatch")
     n_s = len(labels.safe)
@@ -329,7 +328,8 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
         deps[d, :len(dl)] = dl
         n_deps[d] = len(dl)
     sigma = np.ones(n) if monte_carlo else noise.sigma
-    inv_cov = _lib.as_f64(noise.inv_cov if monte_carlo else np.eye(n))
+    inv_cov = _lib.as_f64(noise.inv_cov if monte_carlo and not custom
+                          else np.eye(n))
     arrays = dict(
         counts=counts, eta=_lib.as_f64(state.eta),
         sigma=_lib.as_f64(sigma), inv_cov=inv_cov, edges=edges,
@@ -349,11 +349,11 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
     if monte_carlo:
         # noise.py:63-73 (FullNormal.density), :133-153; abstraction.py:
         # 378-397 (seeded per row and destination from mc_seed)
-        desc.mc = 1
+        desc.mc = 2 if custom else 1
         desc.mc_samples = int(noise.samples)
         desc.mc_seed = int(opts.mc_seed) & (2**64 - 1)
-        desc.mc_norm = (math.sqrt(np.linalg.det(noise.inv_cov))
-                        * (2 * math.pi) ** (-n / 2))
+        desc.mc_norm = 1.0 if custom else (
+            math.sqrt(np.linalg.det(noise.inv_cov)) * (2 * math.pi) ** (-n / 2))
     desc.inv_cov = _lib.ptr(arrays["inv_cov"], _lib.c_dbl)
     for key in ("counts", "safe_multi", "target_multi", "avoid_multi",
                 "deps", "n_deps"):
@@ -364,7 +364,8 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
     desc.n_s = n_s
     desc.n_t = len(labels.target)
     desc.n_a = len(labels.avoid)
-    src = lowered.source.encode()
+    src = (lowered.source + (lower_density(noise.density_expr, n)
+                             if custom else "")).encode()
     desc.dyn_source = src
     desc.n_consts = lowered.consts.shape[1]
     desc.zero_cutoff = opts.zero_cutoff

@@ -116,6 +116,7 @@ std::string config_header(const imp_build_desc* d) {
   o << "#define IMP_N " << d->n << "\n#define IMP_NC "
     << std::max(d->n_consts, 1) << "\n";
   o << "#define IMP_MC " << (d->mc ? 1 : 0) << "\n";
+  o << "#define IMP_MC_CUSTOM " << (d->mc == 2 ? 1 : 0) << "\n";
   o << "#define IMP_MEAN_BLOCK " << nm_block(d->n) << "\n";
   o << "#define IMP_REFINE_BLOCK " << nm_block(d->n) << "\n";
   // tuning knobs (environment overrides for experiments)
@@ -397,6 +398,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     DevBuf<double> g_inv;
     if (d->mc) {
       IMP_REQUIRE(d->inv_cov && d->mc_samples >= 2, "bad Monte Carlo noise");
+      IMP_REQUIRE(d->mc == 1 || d->mc == 2, "bad Monte Carlo noise kind");
       g_inv = upload(d->inv_cov, (size_t)N * N, s);
       P.inv_cov = g_inv.ptr;
     }

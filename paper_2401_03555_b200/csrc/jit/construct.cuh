@@ -793,12 +793,20 @@ struct ImpMc {
 };
 
 __device__ __forceinline__ double imp_mc_density(ImpMc& c) {
+  double y[IMP_N];
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d)
+    y[d] = c.lo[d] + c.w[d] * imp_philox_double(&c.g);
+#if IMP_MC_CUSTOM
+  // CustomNoise.density (noise.py:84-95): the lowered expression over the
+  // point and the mean; non-finite or negative -> NoiseError
+  const double v = imp_density(y, c.mean);
+  if (!imp_finite(v) || v < 0.0) c.bad = true;
+  return v;
+#else
   double diff[IMP_N];
 #pragma unroll
-  for (int d = 0; d < IMP_N; ++d) {
-    const double y = c.lo[d] + c.w[d] * imp_philox_double(&c.g);
-    diff[d] = y - c.mean[d];
-  }
+  for (int d = 0; d < IMP_N; ++d) diff[d] = y[d] - c.mean[d];
   double q = 0.0;   // einsum("ki,ij,kj->k", diff, inv_cov, diff)
 #pragma unroll
   for (int i = 0; i < IMP_N; ++i)
@@ -808,6 +816,7 @@ __device__ __forceinline__ double imp_mc_density(ImpMc& c) {
   const double v = c.P->mc_norm * imp_exp(-0.5 * q);
   if (!imp_finite(v)) c.bad = true;
   return v;
+#endif
 }
 
 // numpy pairwise_sum of the next n densities (PW_BLOCKSIZE 128, 8 lanes):

@@ -441,6 +441,39 @@ def lower_dynamics(dyn: DynamicsSpec, input_reps, disturb_reps):
                            deps=deps)
 
 
+def lower_density(expr, n):
+    """CUDA C of a custom noise density (noise.py:76-95, CustomNoise.density)
+    over one integration point y[0..n) and the mean m[0..n):
+    `__device__ double imp_density(const double* y, const double* m)`.
+    Same AST order as numpy's elementwise evaluation; number literals as
+    exact hex floats; exp is the glibc restatement (imp_exp)."""
+    fns = dict(_CUDA_FN, exp="imp_exp")
+
+    def emit(node):
+        tag = node[0]
+        if tag == "num":
+            return f"({float(node[1]).hex()})"
+        if tag == "var":
+            name = node[1]
+            return f"{'y' if name[0] == 'y' else 'm'}[{int(name[1:]) - 1}]"
+        if tag == "neg":
+            return f"(-{emit(node[1])})"
+        if tag == "bin":
+            a, b = emit(node[2]), emit(node[3])
+            if node[1] == "^":
+                return f"pow({a}, {b})"
+            if node[1] == "/":
+                return f"imp_div({a}, {b})"
+            return f"({a} {node[1]} {b})"
+        if tag == "call":
+            return f"{fns[node[1]]}({', '.join(emit(a) for a in node[2])})"
+        raise ValueError(f"cannot lower {tag}")
+
+    del n
+    return ("__device__ __forceinline__ double imp_density(const double* y, "
+            f"const double* m) {{ return {emit(expr.node)}; }}\n")
+
+
 def _rcp(v):
     """RN(1/v) for imp_div_rcp; NaN outside 2^+-100 (device then divides)."""
     return 1.0 / v if 2.0 ** -100 <= abs(v) <= 2.0 ** 100 else float("nan")

@@ -47,11 +47,37 @@ avoid = (x1 <= 0.5) & (x2 >= 2.5)
 [synthesis]
 seed = 3
 """,
+    "mc2d_custom": """
+[state]
+lb = 0 0
+ub = 3 3
+eta = 1 1
+[input]
+lb = -0.5
+ub = 0.5
+eta = 1
+[dynamics]
+f1 = 0.8*x1 + 0.1*x2 + u1 + 0.3
+f2 = 0.1*x1 + 0.7*x2 + 0.5
+[noise]
+type = custom
+density = exp(-((y1-m1)^2 + (y2-m2)^2) / 0.5) / (0.5*3.141592653589793) * (1 + 0.2*(y1-m1)*(y2-m2)/(1 + (y1-m1)^2 + (y2-m2)^2))
+samples = 128
+[spec]
+type = reach-avoid
+target = (x1 >= 2.5) & (x2 >= 2.5)
+avoid = (x1 <= 0.5) & (x2 >= 2.5)
+[synthesis]
+seed = 5
+""",
 }
 
 
 def main():
+    only = sys.argv[1:]
     for name, text in SYSTEMS.items():
+        if only and name not in only:
+            continue
         with tempfile.NamedTemporaryFile("w", suffix=".cfg", delete=False) as fh:
             fh.write(text)
         cfg = load_config(fh.name)

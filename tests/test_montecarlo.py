@@ -1,7 +1,7 @@
-"""Monte Carlo (full-covariance) noise path.
+"""Monte Carlo noise path: FullNormal and CustomNoise.
 
-Pinning chain: the reference's Monte Carlo abstraction of a small
-full-covariance system (tests/golden/mc_mc2d_full.npz, made by
+Pinning chain: the reference's Monte Carlo abstractions of a small system
+under full-covariance and custom-density noise (tests/golden/mc_*.npz, made by
 make_mc_golden.py) -> the oracle restatement (oracle/montecarlo.py, numpy's
 own random streams, einsum, exp and pairwise mean: bitwise) -> the GPU
 (k_refine with the Monte Carlo objective; numpy's streams restated in
@@ -24,13 +24,17 @@ TOL = 1e-12
 KEYS = ("t_min", "t_max", "r_min", "r_max", "a_min", "a_max")
 
 
-def fixture():
-    g = dict(np.load(os.path.join(G.GOLDEN, "mc_mc2d_full.npz")))
+NAMES = ("mc2d_full", "mc2d_custom")
+
+
+def fixture(name="mc2d_full"):
+    g = dict(np.load(os.path.join(G.GOLDEN, f"mc_{name}.npz")))
     return g, parse_config_text(str(g["config"]))
 
 
-def test_oracle_rows_bitwise_vs_reference():
-    g, cfg = fixture()
+@pytest.mark.parametrize("name", NAMES)
+def test_oracle_rows_bitwise_vs_reference(name):
+    g, cfg = fixture(name)
     rows = [0, 9, 27]
     out = OM.build(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
                    cfg.abstraction_options(), rows=rows)
@@ -39,9 +43,10 @@ def test_oracle_rows_bitwise_vs_reference():
 
 
 @pytest.mark.gpu
-def test_gpu_monte_carlo_abstraction_matches_reference():
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_monte_carlo_abstraction_matches_reference(name):
     from paper_2401_03555_b200 import build_abstraction
-    g, cfg = fixture()
+    g, cfg = fixture(name)
     im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
                            cfg.abstraction_options())
     for k in KEYS:
@@ -51,9 +56,10 @@ def test_gpu_monte_carlo_abstraction_matches_reference():
 
 
 @pytest.mark.gpu
-def test_gpu_monte_carlo_synthesis_matches_oracle():
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_monte_carlo_synthesis_matches_oracle(name):
     from paper_2401_03555_b200 import build_abstraction, synthesize_reach
-    g, cfg = fixture()
+    g, cfg = fixture(name)
     im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
                            cfg.abstraction_options())
     c = synthesize_reach(im, eps=1e-6)
