@@ -129,7 +129,7 @@ std::string config_header(const imp_build_desc* d) {
   o << "#define IMP_NDTR_CHUNK " << (ch ? atoi(ch) : 1) << "\n";
   o << "#define IMP_INST_SMEM " << inst_smem() << "\n";
   const char* batch = getenv("IMPACT_REFINE_BATCH");
-  o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 2) << "\n";
+  o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 4) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
   for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->n_deps[q];
   o << "};\n__device__ constexpr int kDeps[IMP_N][IMP_N] = {";

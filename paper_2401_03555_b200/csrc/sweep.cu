@@ -355,7 +355,10 @@ struct K5Shape {
 #ifndef IMP_K5_WWARP
 #define IMP_K5_WWARP 32
 #endif
-  static constexpr int W = TEAM > 32 ? 32 : IMP_K5_WWARP;
+#ifndef IMP_K5_WCTA
+#define IMP_K5_WCTA 128
+#endif
+  static constexpr int W = TEAM > 32 ? IMP_K5_WCTA : IMP_K5_WWARP;
   static constexpr int WIN = 2 * 2 * W;   // [track][slot] heads
 };
 

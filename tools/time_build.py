@@ -1,22 +1,23 @@
-"""Time one GPU build (+ optional synthesis) of a benchmark config."""
-import sys, time
+"""Time build_abstraction of a benchmark config (second build: JIT cached).
+
+    python tools/time_build.py NAME [once]
+JIT knobs via env: IMPACT_NDTR_CHUNK, IMPACT_REFINE_MINB, IMPACT_REFINE_BATCH,
+IMPACT_INST_SMEM.
+"""
+import sys
 sys.path.insert(0, ".")
-from paper_2401_03555_b200.config import benchmark
 from paper_2401_03555_b200.abstraction import build_abstraction
-import bench
+from paper_2401_03555_b200.config import benchmark
 
 name = sys.argv[1]
-synth = len(sys.argv) > 2 and sys.argv[2] == "synth"
-reps = 1 if len(sys.argv) > 2 and sys.argv[2] == "once" else 2
 cfg = benchmark(name)
-labels = cfg.labels()
-for rep in range(reps):
-    t0 = time.perf_counter()
-    im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels, cfg.abstraction_options())
-    t1 = time.perf_counter()
-    r = im.build_report
-    print(name, f"wall {t1-t0:.2f}s", r, f"evals/s {r.nm_evals/max(r.ms_refine,1e-9)*1e3:.3e}", flush=True)
-if synth:
-    t0 = time.perf_counter()
-    c = bench._spec_call(cfg, im)
-    print("synth", time.perf_counter() - t0, c.meta)
+args = (cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
+        cfg.abstraction_options())
+im = build_abstraction(*args)
+if len(sys.argv) < 3:
+    del im
+    im = build_abstraction(*args)
+r = im.build_report
+print(f"{name}: ms_total={r.ms_total:.1f} ms_refine={r.ms_refine:.1f} "
+      f"evals/s {r.nm_evals / (r.ms_refine * 1e-3):.4g} "
+      f"simt={r.nm_evals / max(r.nm_lane_slots, 1) / 32:.3f}")
