@@ -243,7 +243,10 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    # IMP_BENCH_FORCE_SHARDED=1 runs the sharded (multi-GPU) step even at
+    # world size 1 (to exercise that path on a single-GPU box)
+    sharded_path = world > 1 or os.environ.get("IMP_BENCH_FORCE_SHARDED") == "1"
+    if sharded_path:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
@@ -254,7 +257,7 @@ def run_b200(args):
     n_u = cfg.input_space.total if cfg.input_space is not None else 1
     n_w = cfg.disturb_space.total if cfg.disturb_space is not None else 1
     rows_total = n_s * n_u * n_w
-    if world > 1:
+    if sharded_path:
         return run_sharded(args, cfg, labels, world, rank, device)
 
     _lib.load()
@@ -407,10 +410,12 @@ def _h2d_bytes(cfg, labels):
 
 
 def run_sharded(args, cfg, labels, world, rank, device):
+    import torch.distributed as dist
     from paper_2401_03555_b200 import sharded
     line = sharded.bench_step(args, cfg, labels, world, rank, device)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 # --- reference arm ---------------------------------------------------------------

@@ -199,10 +199,17 @@ def synthesize(engine, dist, spec, mode="pessimistic", eps=1e-6, horizon=None,
             (ph1.iterations, ph2.iterations), (ph1.fallback, ph2.fallback))
 
 
+def _h2d(cfg, labels):
+    from bench import _h2d_bytes
+    return _h2d_bytes(cfg, labels)
+
+
 def bench_step(args, cfg, labels, world, rank, device):
     """bench.py at N > 1: each rank builds its shard, then the sharded
-    two-phase synthesis; device time is the max over ranks (barrier +
-    synchronize around every timed step)."""
+    two-phase synthesis.  Device time (CUDA events on the launching stream,
+    max over ranks) with a barrier + synchronize around every timed step;
+    e2e is the same step through the public API from host inputs to the
+    host controller (wall time, max over ranks)."""
     import time
     import torch
     import torch.distributed as dist
@@ -212,29 +219,47 @@ def bench_step(args, cfg, labels, world, rank, device):
     n_w = cfg.disturb_space.total if cfg.disturb_space is not None else 1
     k_range = shard_range(n_s, world, rank)
     spec = "safety" if cfg.spec_type == "safety" else "reach"
-    builds, synths, sweeps = [], [], []
+    builds, synths, sweeps, walls = [], [], [], []
+    sampler = None
+    if rank == 0:
+        from bench import ClockSampler
+        sampler = ClockSampler(device)
+    l0 = None
+    ctrl_bytes = 0
     for step in range(args.warmup + args.steps):
+        timed = step >= args.warmup
+        if timed and l0 is None:
+            if sampler:
+                sampler.start()
+            l0 = _lib.launch_count()
         dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        w0 = time.perf_counter()
         imdp = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels,
                                  cfg.abstraction_options(), device=device,
                                  k_range=k_range)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
         eng = CudaShard(imdp, device)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e1.record()
         res = synthesize(eng, dist, spec, cfg.mode, cfg.eps, cfg.horizon,
                          cfg.max_iterations)
+        e2.record()
         torch.cuda.synchronize()
-        t2 = time.perf_counter()
-        if step >= args.warmup:
+        w1 = time.perf_counter()
+        if timed:
             builds.append(imdp.build_report.ms_total)
-            synths.append((t2 - t1) * 1e3)
+            synths.append(e1.elapsed_time(e2))
             sweeps.append(res[3][0])
-    mx = torch.tensor([np.mean(builds), np.mean(synths)], dtype=torch.float64,
-                      device=torch.device("cuda", device))
+            walls.append((w1 - w0) * 1e3)
+            ctrl_bytes = sum(np.asarray(a).nbytes for a in res[:3]
+                             if a is not None)
+    l1 = _lib.launch_count()
+    clocks = sampler.stop() if sampler else None
+    mx = torch.tensor([np.mean(builds), np.mean(synths), np.mean(walls)],
+                      dtype=torch.float64, device=torch.device("cuda", device))
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    ms_build, ms_synth = (float(x) for x in mx.cpu().tolist())
+    ms_build, ms_synth, ms_wall = (float(x) for x in mx.cpu().tolist())
     entries = n_s * n_u * n_w * n_s
     if rank != 0:
         return None
@@ -247,8 +272,16 @@ def bench_step(args, cfg, labels, world, rank, device):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.config, "rows": n_s * n_u * n_w,
-                   "n_s": n_s, "parallelism": f"states sharded over {world}"
-                   " ranks; V all-gathered per sweep (NCCL)"},
+                   "n_s": n_s, "entries": entries,
+                   "step": "build_abstraction (shard) + two-phase synthesis",
+                   "parallelism": f"states sharded over {world} ranks; V "
+                                  "all-gathered per sweep (NCCL)"},
         "sweeps_per_s": float(np.mean(sweeps)) / (ms_synth * 1e-3),
         "ms_build": ms_build, "ms_synthesis": ms_synth,
+        "e2e": {"value": entries / (ms_wall * 1e-3), "unit": "entries/s",
+                "h2d_bytes_per_step": _h2d(cfg, labels),
+                "d2h_bytes_per_step": int(ctrl_bytes),
+                "ms_per_step_wall": ms_wall},
+        "clocks": clocks,
+        "gpu_launches": int(l1[0] - l0[0]),
     }
