@@ -145,6 +145,11 @@ typedef struct imp_build_desc {
   uint64_t mc_seed;
   double mc_norm;            /* sqrt(det(inv_cov)) * (2 pi)^(-n/2), numpy  */
   const double* inv_cov;     /* (n, n)                                      */
+  /* clipped cell bounds of every lattice coordinate, dimension-major
+   * (sum(counts)): lets separable dynamics compute one mean range / table
+   * per (dimension, coordinate, input, disturbance); NULL: per row */
+  const double* dim_lo;
+  const double* dim_hi;
 } imp_build_desc;
 
 /* Per-build timings (device milliseconds, CUDA events) and counters. */

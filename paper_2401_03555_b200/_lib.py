@@ -52,7 +52,7 @@ class BuildDesc(ctypes.Structure):
                 ("k_begin", c_i32), ("k_count", c_i32),
                 ("mc", c_i32), ("mc_samples", c_i32),
                 ("mc_seed", ctypes.c_uint64), ("mc_norm", c_dbl),
-                ("inv_cov", P_dbl)]
+                ("inv_cov", P_dbl), ("dim_lo", P_dbl), ("dim_hi", P_dbl)]
 
 
 class BuildStats(ctypes.Structure):

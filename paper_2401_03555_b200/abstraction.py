@@ -322,6 +322,13 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
     rep = state.lb + safe_multi * state.eta
     src_lo = _lib.as_f64(np.maximum(rep - state.eta / 2, state.lb))
     src_hi = _lib.as_f64(np.minimum(rep + state.eta / 2, state.ub))
+    # the same clipped cells per lattice coordinate (elementwise the same
+    # float64 operations), for the per-coordinate separable tables
+    dim_lo, dim_hi = [], []
+    for d in range(n):
+        rep_d = state.lb[d] + np.arange(state.counts[d]) * state.eta[d]
+        dim_lo.append(np.maximum(rep_d - state.eta[d] / 2, state.lb[d]))
+        dim_hi.append(np.minimum(rep_d + state.eta[d] / 2, state.ub[d]))
     deps = np.full((n, n), -1, dtype=np.int32)
     n_deps = np.zeros(n, dtype=np.int32)
     for d, dl in enumerate(lowered.deps):
@@ -340,6 +347,8 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
         avoid_multi=_lib.as_i32(multi_indices(state, labels.avoid)
                                 .reshape(-1, n)),
         src_lo=src_lo, src_hi=src_hi, consts=_lib.as_f64(lowered.consts),
+        dim_lo=_lib.as_f64(np.concatenate(dim_lo)),
+        dim_hi=_lib.as_f64(np.concatenate(dim_hi)),
         deps=_lib.as_i32(deps), n_deps=_lib.as_i32(n_deps))
     desc = _lib.BuildDesc()
     desc.device = device
@@ -359,7 +368,7 @@ def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):
                 "deps", "n_deps"):
         setattr(desc, key, _lib.ptr(arrays[key], _lib.c_i32))
     for key in ("eta", "sigma", "edges", "cover_lo", "cover_hi", "src_lo",
-                "src_hi", "consts"):
+                "src_hi", "consts", "dim_lo", "dim_hi"):
         setattr(desc, key, _lib.ptr(arrays[key], _lib.c_dbl))
     desc.n_s = n_s
     desc.n_t = len(labels.target)

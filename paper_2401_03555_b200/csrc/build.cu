@@ -75,6 +75,11 @@ struct BuildParams {
   double* err_val;
   double sig[16];
   double sig_rcp[16];
+  int sep;
+  const double* dim_lo;
+  const double* dim_hi;
+  double* sep_mr;
+  double* sep_tab;
   long long row0;
   int mc_samples;
   unsigned long long mc_seed;
@@ -88,7 +93,7 @@ struct BuildParams {
 struct JitModule {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t mean = nullptr, outer = nullptr, refine = nullptr,
-               assemble = nullptr, simulate = nullptr;
+               assemble = nullptr, simulate = nullptr, sep_tables = nullptr;
 };
 
 std::mutex g_jit_mu;
@@ -201,6 +206,7 @@ JitModule& jit(int device, const std::string& config, const std::string& dyn) {
   IMP_CUDA(cudaLibraryGetKernel(&m.refine, m.lib, "k_refine"));
   IMP_CUDA(cudaLibraryGetKernel(&m.assemble, m.lib, "k_assemble"));
   IMP_CUDA(cudaLibraryGetKernel(&m.simulate, m.lib, "k_simulate"));
+  IMP_CUDA(cudaLibraryGetKernel(&m.sep_tables, m.lib, "k_sep_tables"));
   return g_jit_cache.emplace(key, m).first->second;
 }
 
@@ -268,7 +274,6 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     IMP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{s};
     Events ev;
-    IMP_CUDA(cudaEventRecord(ev.e[0], s));
 
     // --- host geometry -> device ------------------------------------------
     std::vector<int> edge_off(N), strides(N);
@@ -420,7 +425,45 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     const size_t nm_doubles = (size_t)(N + 4) * N + (N + 1);
     const size_t inst_bytes = 5 * 8 + 5 * 4 + 4 + 2 * N * 8 + (d->mc ? 8 : 0);
     const int block1 = nm_block(N);
-    if (n_rows > 0 && !d->mc) {
+    // separable dynamics: one table per (dimension, coordinate, input,
+    // disturbance) instead of per row, when that is fewer (always, in
+    // practice) and the tables fit comfortably
+    long long nkeys = 0, tab_doubles = 0;
+    for (int q = 0; q < N; ++q) {
+      nkeys += (long long)d->counts[q] * d->n_u * d->n_w;
+      tab_doubles += 2ll * d->counts[q] * d->counts[q] * d->n_u * d->n_w;
+    }
+    const bool sep = d->separable && !d->mc && d->dim_lo && d->dim_hi &&
+                     getenv("IMPACT_SEP_TABLES") == nullptr &&
+                     nkeys < n_rows * N && tab_doubles < (1ll << 29);
+    DevBuf<double> g_dlo, g_dhi, sep_mr, sep_tab;
+    P.sep = sep ? 1 : 0;
+    if (sep && n_rows > 0) {
+      int csum = 0;
+      for (int q = 0; q < N; ++q) csum += d->counts[q];
+      g_dlo = upload(d->dim_lo, csum, s);
+      g_dhi = upload(d->dim_hi, csum, s);
+      sep_mr.alloc(2 * nkeys);
+      sep_tab.alloc(std::max<long long>(tab_doubles, 1));
+      P.dim_lo = g_dlo.ptr;
+      P.dim_hi = g_dhi.ptr;
+      P.sep_mr = sep_mr.ptr;
+      P.sep_tab = sep_tab.ptr;
+    }
+    // device timing starts here: host geometry, uploads and allocations
+    // above are part of the end-to-end time, not of the kernels'
+    IMP_CUDA(cudaEventRecord(ev.e[0], s));
+    if (sep && n_rows > 0) {
+      P.write = 0;   // mean ranges, one thread per (key, sign)
+      unsigned grid = (unsigned)std::min<long long>(
+          (2 * nkeys + block1 - 1) / block1, (long long)sms * 64);
+      launch(M.sep_tables, grid, block1, block1 * nm_doubles * 8, s, P);
+      P.write = 1;   // tables, one thread per (key, bin)
+      grid = (unsigned)std::min<long long>(
+          (tab_doubles / 2 + block1 - 1) / block1, (long long)sms * 64);
+      launch(M.sep_tables, grid, block1, block1 * nm_doubles * 8, s, P);
+    }
+    if (n_rows > 0 && !d->mc && !sep) {
       const long long ntask = n_rows * N * 2;
       unsigned grid = (unsigned)std::min<long long>((ntask + block1 - 1) / block1,
                                                     (long long)sms * 64);

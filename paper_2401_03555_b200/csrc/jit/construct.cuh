@@ -100,6 +100,12 @@ struct BuildParams {
   // and RN(1/sigma) for imp_div_rcp (NaN when sigma is outside 2^+-100)
   double sig[16];
   double sig_rcp[16];
+  // separable dynamics: per-key mean ranges and 1-D tables (k_sep_tables)
+  int sep;
+  const double* dim_lo;       // (sum counts) clipped coordinate cells
+  const double* dim_hi;
+  double* sep_mr;             // (keys, 2)
+  double* sep_tab;            // per key: counts[d] x {min, max}
   // Monte Carlo noise (IMP_MC modules)
   long long row0;             // global index of local row 0 (seeding)
   int mc_samples;
@@ -320,21 +326,23 @@ __device__ __forceinline__ void imp_flag_nonfinite(const BuildParams& P,
 // Stage 1: per-dimension mean ranges (abstraction.py:256-284)
 // ---------------------------------------------------------------------------
 
+// min (sgn 0) or max (sgn 1) of f_DI over the dependency sub-cell
+// [lo, hi] (the source cell's coordinates of kDeps[DI]) with folded
+// constants K; `flag_row` is reported if f is non-finite.  Returns the
+// number of objective evaluations.
 template <int DI>
-__device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
-                                   double* smem, int S) {
+__device__ long long imp_mean_box(const BuildParams& P, const double* K,
+                                  const double* lo, const double* hi, int sgn,
+                                  long long flag_row, double* smem, int S,
+                                  double* out) {
   constexpr int D = kNDeps[DI];
-  int k, j, i;
-  imp_row_kji(P, r, k, j, i);
-  const double* K = P.consts + (long long)(j * P.n_w + i) * IMP_NC;
   double xfull[IMP_N];
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) xfull[d] = 0.0;
   if constexpr (D == 0) {
     double v = imp_fd(DI, xfull, K);
-    if (!imp_finite(v)) imp_flag_nonfinite(P, r);
-    if (sgn == 0) P.mlo[r * IMP_N + DI] = v;
-    else P.mhi[r * IMP_N + DI] = v;
+    if (!imp_finite(v)) imp_flag_nonfinite(P, flag_row);
+    *out = v;
     return 0;
   } else {
     NelderMead<D, IMP_MEAN_BLOCK> nm;
@@ -344,8 +352,8 @@ __device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
     nm.max_evals = imp_max_evals(P, D);
 #pragma unroll
     for (int q = 0; q < D; ++q) {
-      nm.lo[q] = P.src_lo[(long long)k * IMP_N + kDeps[DI][q]];
-      nm.hi[q] = P.src_hi[(long long)k * IMP_N + kDeps[DI][q]];
+      nm.lo[q] = lo[q];
+      nm.hi[q] = hi[q];
     }
     const int ms = imp_multistart(P, D);
     const double sign = sgn ? -1.0 : 1.0;
@@ -362,7 +370,7 @@ __device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
         for (int q = 0; q < D; ++q) xfull[kDeps[DI][q]] = p[q];
         double val = imp_fd(DI, xfull, K) * sign;
         if (!imp_finite(val)) {
-          imp_flag_nonfinite(P, r);
+          imp_flag_nonfinite(P, flag_row);
           val = 0.0;
         }
         nm.feed(val);
@@ -370,10 +378,126 @@ __device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
       }
       best = fmin(best, nm.best);
     }
-    if (sgn == 0) P.mlo[r * IMP_N + DI] = best;
-    else P.mhi[r * IMP_N + DI] = -best;
+    *out = sgn ? -best : best;
     return ev;
   }
+}
+
+template <int DI>
+__device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
+                                   double* smem, int S) {
+  constexpr int D = kNDeps[DI];
+  int k, j, i;
+  imp_row_kji(P, r, k, j, i);
+  const double* K = P.consts + (long long)(j * P.n_w + i) * IMP_NC;
+  double lo[D > 0 ? D : 1], hi[D > 0 ? D : 1];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    lo[q] = P.src_lo[(long long)k * IMP_N + kDeps[DI][q]];
+    hi[q] = P.src_hi[(long long)k * IMP_N + kDeps[DI][q]];
+  }
+  double v;
+  const long long ev = imp_mean_box<DI>(P, K, lo, hi, sgn, r, smem, S, &v);
+  if (sgn == 0) P.mlo[r * IMP_N + DI] = v;
+  else P.mhi[r * IMP_N + DI] = v;
+  return ev;
+}
+
+// --- separable dynamics: tables per (dimension, coordinate, input, dist.) --
+// f_d depends on x_d alone, so a row's mean range and 1-D extremes table
+// in dimension d are functions of (d, c_d(k), j, i) only: k_sep_tables
+// computes each once (the same NM and interval probabilities, hence the
+// same bits) and k_outer gathers them per row instead of recomputing them
+// (robot2d_reachavoid: 41 x 441 keys per dimension vs 694 575 rows).
+__device__ __forceinline__ long long imp_sep_key(const BuildParams& P, int d,
+                                                 int c, int j, int i) {
+  long long off = 0;
+  for (int e = 0; e < d; ++e) off += (long long)P.counts[e] * P.n_u * P.n_w;
+  return off + ((long long)c * P.n_u + j) * P.n_w + i;
+}
+
+__device__ __forceinline__ long long imp_sep_tab(const BuildParams& P, int d,
+                                                 int c, int j, int i) {
+  long long off = 0;
+  for (int e = 0; e < d; ++e)
+    off += 2ll * P.counts[e] * P.counts[e] * P.n_u * P.n_w;
+  return off + (((long long)c * P.n_u + j) * P.n_w + i) * 2 * P.counts[d];
+}
+
+template <int DI>
+__device__ __forceinline__ long long imp_sep_dispatch(
+    int d, const BuildParams& P, const double* K, const double* lo,
+    const double* hi, int sgn, double* smem, int S, double* out) {
+  if constexpr (DI < IMP_N) {
+    if (d == DI) return imp_mean_box<DI>(P, K, lo, hi, sgn, 0, smem, S, out);
+    return imp_sep_dispatch<DI + 1>(d, P, K, lo, hi, sgn, smem, S, out);
+  }
+  return 0;
+}
+
+// P.write == 0: one thread per (key, sign) -> mean ranges sep_mr;
+// P.write == 1: one thread per (key, bin) -> the 1-D extremes table
+extern "C" __global__ void __launch_bounds__(IMP_MEAN_BLOCK)
+    k_sep_tables(BuildParams P) {
+  extern __shared__ double smem[];
+  constexpr int S = IMP_MEAN_BLOCK;
+  long long nkeys = 0, nbins = 0;
+  for (int e = 0; e < IMP_N; ++e) {
+    nkeys += (long long)P.counts[e] * P.n_u * P.n_w;
+    nbins += (long long)P.counts[e] * P.counts[e] * P.n_u * P.n_w;
+  }
+  unsigned long long ev = 0;
+  const long long ntask = P.write ? nbins : 2 * nkeys;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       t < ntask; t += (long long)gridDim.x * blockDim.x) {
+    // task -> (d, key within d, bin or sign)
+    int d = 0, coord0 = 0;
+    long long rem = P.write ? t : t >> 1, koff = 0;
+    for (;;) {
+      const long long kd = (long long)P.counts[d] * P.n_u * P.n_w;
+      const long long per = P.write ? kd * P.counts[d] : kd;
+      if (rem < per) break;
+      rem -= per;
+      koff += kd;
+      coord0 += P.counts[d];
+      ++d;
+    }
+    int q = 0;
+    if (P.write) {
+      q = (int)(rem % P.counts[d]);
+      rem /= P.counts[d];
+    }
+    const int i = (int)(rem % P.n_w);
+    const long long rest = rem / P.n_w;
+    const int j = (int)(rest % P.n_u);
+    const int c = (int)(rest / P.n_u);
+    const long long kk = koff + rem;
+    if (!P.write) {
+      const double* K = P.consts + (long long)(j * P.n_w + i) * IMP_NC;
+      const double lo = P.dim_lo[coord0 + c], hi = P.dim_hi[coord0 + c];
+      const int sgn = (int)(t & 1);
+      double v;
+      ev += imp_sep_dispatch<0>(d, P, K, &lo, &hi, sgn, smem + threadIdx.x,
+                                S, &v);
+      P.sep_mr[2 * kk + sgn] = v;
+    } else {
+      // exact 1-D extremes (abstraction.py:287-297), as k_outer computes
+      const double ml = P.sep_mr[2 * kk], mh = P.sep_mr[2 * kk + 1];
+      const double* e = P.edges + P.edge_off[d];
+      const double sg = P.sigma[d];
+      const double plo = imp_interval_prob(sg, ml, e[q], e[q + 1]);
+      const double phi = imp_interval_prob(sg, mh, e[q], e[q + 1]);
+      const double mid = (e[q] + e[q + 1]) / 2;
+      double top;
+      if (mid < ml) top = plo;
+      else if (mid > mh) top = phi;
+      else top = imp_interval_prob(sg, 0.0, -P.eta[d] / 2, P.eta[d] / 2);
+      double* tab = P.sep_tab + imp_sep_tab(P, d, c, j, i);
+      tab[2 * q] = fmin(plo, phi);
+      tab[2 * q + 1] = top;
+    }
+  }
+  if (ev) atomicAdd((unsigned long long*)P.evals, ev);
 }
 
 template <int DI>
@@ -452,22 +576,49 @@ extern "C" __global__ void k_outer(BuildParams P) {
   __shared__ double red[32];
   __shared__ int wsum[32];
   __shared__ int s_blo[IMP_N], s_bext[IMP_N];
+  __shared__ int s_lo[IMP_N], s_hi[IMP_N];
+  __shared__ unsigned long long s_pm[IMP_N];
   __shared__ double s_ml[IMP_N], s_mh[IMP_N];
+  __shared__ double s_cov[3 * IMP_N];
   int nbins = 0;
   for (int d = 0; d < IMP_N; ++d) nbins += P.counts[d];
   double* gmin = smem;
   double* gmax = smem + nbins;
 
   for (long long r = blockIdx.x; r < P.n_rows; r += gridDim.x) {
+    int rk, rj, ri;
+    imp_row_kji(P, r, rk, rj, ri);
+    const int rflat = P.sep ? P.safe_flat[rk] : 0;
     if (threadIdx.x < IMP_N) {
-      s_ml[threadIdx.x] = P.mlo[r * IMP_N + threadIdx.x];
-      s_mh[threadIdx.x] = P.mhi[r * IMP_N + threadIdx.x];
+      if (P.sep) {
+        const int d = threadIdx.x;
+        const int c = (rflat / P.strides[d]) % P.counts[d];
+        const long long kk = imp_sep_key(P, d, c, rj, ri);
+        s_ml[d] = P.sep_mr[2 * kk];
+        s_mh[d] = P.sep_mr[2 * kk + 1];
+      } else {
+        s_ml[threadIdx.x] = P.mlo[r * IMP_N + threadIdx.x];
+        s_mh[threadIdx.x] = P.mhi[r * IMP_N + threadIdx.x];
+      }
     }
     __syncthreads();
+    if (P.sep) {   // separable: gather this row's tables (k_sep_tables)
+      int d = 0, base = 0;
+      for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+        while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
+        const int c = (rflat / P.strides[d]) % P.counts[d];
+        const double* tab = P.sep_tab + imp_sep_tab(P, d, c, rj, ri);
+        const int q = b - base;
+        gmin[b] = tab[2 * q];
+        gmax[b] = tab[2 * q + 1];
+        d = 0;
+        base = 0;
+      }
+    }
     // exact per-dimension extremes (abstraction.py:287-297); Monte Carlo
     // rows have no closed form: every destination is an NM item
     // (abstraction.py:511-540)
-    if (!IMP_MC) {
+    if (!IMP_MC && !P.sep) {
       int d = 0, base = 0;
       for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
         while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
@@ -491,47 +642,68 @@ extern "C" __global__ void k_outer(BuildParams P) {
     // pruned box: a lattice point can only pass the cutoff if every factor
     // exceeds cutoff / prod_{e != d} max gmax_e (factors are <= 1); the
     // superlevel sets of the unimodal gmax_d are index intervals.
-    if (threadIdx.x == 0 && IMP_MC) {
-      for (int d = 0; d < IMP_N; ++d) {
-        s_blo[d] = 0;
-        s_bext[d] = P.counts[d];
+    // Block-parallel: per-dimension maxima, then the index intervals, with
+    // shared-memory integer atomics (exact: order-free max / min).
+    if (IMP_MC) {
+      if (threadIdx.x < IMP_N) {
+        s_blo[threadIdx.x] = 0;
+        s_bext[threadIdx.x] = P.counts[threadIdx.x];
       }
-    } else if (threadIdx.x == 0) {
-      double pm[IMP_N];
-      int base = 0;
-      for (int d = 0; d < IMP_N; ++d) {
-        double m = 0.0;
-        for (int q = 0; q < P.counts[d]; ++q) m = fmax(m, gmax[base + q]);
-        pm[d] = m;
-        base += P.counts[d];
+      __syncthreads();
+    } else {
+      if (threadIdx.x < IMP_N) {
+        s_pm[threadIdx.x] = 0ull;
+        s_lo[threadIdx.x] = P.counts[threadIdx.x];
+        s_hi[threadIdx.x] = -1;
       }
-      base = 0;
-      for (int d = 0; d < IMP_N; ++d) {
-        double rest = 1.0;
-        for (int e = 0; e < IMP_N; ++e)
-          if (e != d) rest *= pm[e];
-        const double thr = P.cutoff * (1.0 - 1e-9) / rest;
-        int lo = P.counts[d], hi = -1;
-        for (int q = 0; q < P.counts[d]; ++q)
-          if (gmax[base + q] > thr) { lo = min(lo, q); hi = q; }
-        s_blo[d] = lo;
-        s_bext[d] = hi >= lo ? hi - lo + 1 : 0;
-        base += P.counts[d];
+      __syncthreads();
+      {   // pm_d = max_q gmax_d[q] (gmax >= 0: bit order = value order)
+        int d = 0, base = 0;
+        for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+          while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
+          const double gm = gmax[b] > 0.0 ? gmax[b] : 0.0;
+          atomicMax(&s_pm[d], (unsigned long long)__double_as_longlong(gm));
+          d = 0;
+          base = 0;
+        }
       }
+      __syncthreads();
+      {   // superlevel interval of gmax_d above cutoff / prod_{e != d} pm_e
+        int d = 0, base = 0;
+        for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+          while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
+          double rest = 1.0;
+          for (int e = 0; e < IMP_N; ++e)
+            if (e != d) rest *= __longlong_as_double((long long)s_pm[e]);
+          const double thr = P.cutoff * (1.0 - 1e-9) / rest;
+          if (gmax[b] > thr) {
+            atomicMin(&s_lo[d], b - base);
+            atomicMax(&s_hi[d], b - base);
+          }
+          d = 0;
+          base = 0;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < IMP_N) {
+        const int d = threadIdx.x;
+        s_blo[d] = s_lo[d];
+        s_bext[d] = s_hi[d] >= s_lo[d] ? s_hi[d] - s_lo[d] + 1 : 0;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    long long box = 1;
+    int box = 1;   // < 2^31: a sub-box of the state lattice
     for (int d = 0; d < IMP_N; ++d) box *= s_bext[d];
 
     // --- safe destinations: t entries ------------------------------------
     long long out = P.write ? P.row_ptr[r] : 0;
     long long cnt = 0;
-    for (long long q0 = 0; q0 < box; q0 += blockDim.x) {
-      const long long q = q0 + threadIdx.x;
+    for (int q0 = 0; q0 < box; q0 += blockDim.x) {
+      const int q = q0 + threadIdx.x;
       int live = 0, pos = -1;
       double tmin = 0.0, tmax = 0.0;
       if (q < box) {
-        long long rem = q;
+        int rem = q;
         int flat = 0;
         int bidx[IMP_N];
 #pragma unroll
@@ -610,16 +782,23 @@ extern "C" __global__ void k_outer(BuildParams P) {
       const double r1 = imp_block_sum(rs[1], red);
       const double a0 = imp_block_sum(as[0], red);
       const double a1 = imp_block_sum(as[1], red);
+      // cover leak (abstraction.py:300-309): per-dimension factors in
+      // parallel, products in dimension order on thread 0
+      if (threadIdx.x < IMP_N) {
+        const int d = threadIdx.x;
+        const double lo = P.cover_lo[d], hi = P.cover_hi[d];
+        const double mu = imp_clip((lo + hi) / 2, s_ml[d], s_mh[d]);
+        const double s = P.sigma[d];
+        s_cov[3 * d] = imp_interval_prob(s, mu, lo, hi);
+        s_cov[3 * d + 1] = imp_interval_prob(s, s_ml[d], lo, hi);
+        s_cov[3 * d + 2] = imp_interval_prob(s, s_mh[d], lo, hi);
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        // cover leak (abstraction.py:300-309)
         double pmax = 1.0, pmin = 1.0;
         for (int d = 0; d < IMP_N; ++d) {
-          const double lo = P.cover_lo[d], hi = P.cover_hi[d];
-          const double mu = imp_clip((lo + hi) / 2, s_ml[d], s_mh[d]);
-          const double s = P.sigma[d];
-          const double pa = imp_interval_prob(s, mu, lo, hi);
-          const double pl = imp_interval_prob(s, s_ml[d], lo, hi);
-          const double ph = imp_interval_prob(s, s_mh[d], lo, hi);
+          const double pa = s_cov[3 * d], pl = s_cov[3 * d + 1],
+                       ph = s_cov[3 * d + 2];
           pmax = d == 0 ? pa : pmax * pa;
           pmin = d == 0 ? fmin(pl, ph) : pmin * fmin(pl, ph);
         }
