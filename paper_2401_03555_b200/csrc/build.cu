@@ -93,7 +93,8 @@ struct BuildParams {
 struct JitModule {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t mean = nullptr, outer = nullptr, refine = nullptr,
-               assemble = nullptr, simulate = nullptr, sep_tables = nullptr;
+               assemble = nullptr, simulate = nullptr, sep_tables = nullptr,
+               outer_sep = nullptr;
 };
 
 std::mutex g_jit_mu;
@@ -207,6 +208,7 @@ JitModule& jit(int device, const std::string& config, const std::string& dyn) {
   IMP_CUDA(cudaLibraryGetKernel(&m.assemble, m.lib, "k_assemble"));
   IMP_CUDA(cudaLibraryGetKernel(&m.simulate, m.lib, "k_simulate"));
   IMP_CUDA(cudaLibraryGetKernel(&m.sep_tables, m.lib, "k_sep_tables"));
+  IMP_CUDA(cudaLibraryGetKernel(&m.outer_sep, m.lib, "k_outer_sep"));
   return g_jit_cache.emplace(key, m).first->second;
 }
 
@@ -426,8 +428,11 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     const size_t inst_bytes = 5 * 8 + 5 * 4 + 4 + 2 * N * 8 + (d->mc ? 8 : 0);
     const int block1 = nm_block(N);
     // separable dynamics: one table per (dimension, coordinate, input,
-    // disturbance) instead of per row, when that is fewer (always, in
-    // practice) and the tables fit comfortably
+    // disturbance) instead of per row.  The choice depends on the system
+    // only (never on the shard), because it selects k_outer_sep, whose r / a
+    // sums use a warp tree: every shard of a system must take the same path
+    // for the bits to be shard-independent.  (IMPACT_SEP_TABLES set: per-row
+    // path, for A/B timing only.)
     long long nkeys = 0, tab_doubles = 0;
     for (int q = 0; q < N; ++q) {
       nkeys += (long long)d->counts[q] * d->n_u * d->n_w;
@@ -435,7 +440,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     }
     const bool sep = d->separable && !d->mc && d->dim_lo && d->dim_hi &&
                      getenv("IMPACT_SEP_TABLES") == nullptr &&
-                     nkeys < n_rows * N && tab_doubles < (1ll << 29);
+                     tab_doubles < (1ll << 29);
     DevBuf<double> g_dlo, g_dhi, sep_mr, sep_tab;
     P.sep = sep ? 1 : 0;
     if (sep && n_rows > 0) {
@@ -478,8 +483,16 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     const size_t smem2 = 2 * (size_t)nbins * sizeof(double);
     const unsigned grid2 = (unsigned)std::max<long long>(
         1, std::min<long long>(n_rows, (long long)sms * 32));
+    // separable rows with per-key tables: one warp per row
+    const unsigned grid_sep = (unsigned)std::max<long long>(
+        1, std::min<long long>((n_rows * 32 + 255) / 256, (long long)sms * 64));
+    auto outer = [&]() {
+      if (n_rows <= 0) return;
+      if (sep) launch(M.outer_sep, grid_sep, 256, 0, s, P);
+      else launch(M.outer, grid2, 128, smem2, s, P);
+    };
     P.write = 0;
-    if (n_rows > 0) launch(M.outer, grid2, 128, smem2, s, P);
+    outer();
     stage_done("outer count");
     exclusive_scan(tcnt.ptr, reinterpret_cast<long long*>(row_ptr.ptr), n_rows + 1, s);
     exclusive_scan(xcnt.ptr, aux_ptr.ptr, n_rows + 1, s);
@@ -503,7 +516,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     P.aux_min = aux_min.ptr;
     P.aux_max = aux_max.ptr;
     P.write = 1;
-    if (n_rows > 0) launch(M.outer, grid2, 128, smem2, s, P);
+    outer();
     stage_done("outer write");
     IMP_CUDA(cudaEventRecord(ev.e[2], s));
 

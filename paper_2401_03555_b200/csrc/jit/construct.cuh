@@ -815,6 +815,166 @@ extern "C" __global__ void k_outer(BuildParams P) {
   }
 }
 
+// Separable rows, one warp per row (k_outer's work without block barriers):
+// the row's 1-D tables are gathered from k_sep_tables' output (L1/L2 hot),
+// the pruned box is found with warp max / ballots, lattice points are
+// compacted with ballot + popc, and the target / avoid sums use the warp's
+// fixed xor tree.  P.write = 0: counts; 1: CSR values, r / a sums, leak.
+extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = w0; r < P.n_rows; r += nw) {
+    int rk, rj, ri;
+    imp_row_kji(P, r, rk, rj, ri);
+    const int rflat = P.safe_flat[rk];
+    const double* tab[IMP_N];
+    double ml[IMP_N], mh[IMP_N];
+    int cnt_d[IMP_N];
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d) {
+      const int c = (rflat / P.strides[d]) % P.counts[d];
+      tab[d] = P.sep_tab + imp_sep_tab(P, d, c, rj, ri);
+      const long long kk = imp_sep_key(P, d, c, rj, ri);
+      ml[d] = P.sep_mr[2 * kk];
+      mh[d] = P.sep_mr[2 * kk + 1];
+      cnt_d[d] = P.counts[d];
+    }
+    // pm_d = max gmax_d (exact), then the superlevel index interval
+    double pm[IMP_N];
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d) {
+      double m = 0.0;
+      for (int q = lane; q < cnt_d[d]; q += 32) m = fmax(m, tab[d][2 * q + 1]);
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      pm[d] = m;
+    }
+    int blo[IMP_N], bext[IMP_N];
+    int box = 1;
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d) {
+      double rest = 1.0;
+#pragma unroll
+      for (int e = 0; e < IMP_N; ++e)
+        if (e != d) rest *= pm[e];
+      const double thr = P.cutoff * (1.0 - 1e-9) / rest;
+      int lo = cnt_d[d], hi = -1;
+      for (int q0 = 0; q0 < cnt_d[d]; q0 += 32) {
+        const int q = q0 + lane;
+        const unsigned b = __ballot_sync(0xffffffffu,
+                                         q < cnt_d[d] && tab[d][2 * q + 1] > thr);
+        if (b) {
+          lo = min(lo, q0 + __ffs(b) - 1);
+          hi = q0 + 31 - __clz(b);
+        }
+      }
+      blo[d] = lo;
+      bext[d] = hi >= lo ? hi - lo + 1 : 0;
+      box *= bext[d];
+    }
+    // safe destinations
+    long long out = P.write ? P.row_ptr[r] : 0;
+    long long cnt = 0;
+    for (int q0 = 0; q0 < box; q0 += 32) {
+      const int q = q0 + lane;
+      int live = 0, pos = -1;
+      double tmin = 0.0, tmax = 0.0;
+      if (q < box) {
+        int rem = q, flat = 0;
+        int bidx[IMP_N];
+#pragma unroll
+        for (int d = IMP_N - 1; d >= 0; --d) {
+          const int b = blo[d] + rem % bext[d];
+          rem /= bext[d];
+          bidx[d] = b;
+          flat += b * P.strides[d];
+        }
+        pos = P.label ? P.label[flat] : flat;
+        if (pos >= 0) {
+#pragma unroll
+          for (int d = 0; d < IMP_N; ++d) {
+            const double a = tab[d][2 * bidx[d] + 1], c = tab[d][2 * bidx[d]];
+            tmax = d == 0 ? a : tmax * a;
+            tmin = d == 0 ? c : tmin * c;
+          }
+          live = tmax > P.cutoff;
+        }
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, live);
+      if (P.write && live) {
+        const long long at = out + cnt + __popc(b & ((1u << lane) - 1u));
+        P.col[at] = pos;
+        P.lo[at] = fmin(tmin, tmax);
+        P.hi[at] = tmax;
+      }
+      cnt += __popc(b);
+    }
+    if (!P.write) {
+      if (lane == 0) P.t_count[r] = cnt;
+      continue;
+    }
+    // target / avoid masses (full lists) and the cover leak
+    double rs0 = 0.0, rs1 = 0.0, as0 = 0.0, as1 = 0.0;
+    for (int kind = 0; kind < 2; ++kind) {
+      const int n_list = kind == 0 ? P.n_t : P.n_a;
+      const int* flats = kind == 0 ? P.target_flat : P.avoid_flat;
+      for (int q = lane; q < n_list; q += 32) {
+        const int flat = flats[q];
+        double tmin = 0.0, tmax = 0.0;
+#pragma unroll
+        for (int d = 0; d < IMP_N; ++d) {
+          const int bb = (flat / P.strides[d]) % P.counts[d];
+          const double a = tab[d][2 * bb + 1], c = tab[d][2 * bb];
+          tmax = d == 0 ? a : tmax * a;
+          tmin = d == 0 ? c : tmin * c;
+        }
+        if (kind == 0) { rs0 += tmin; rs1 += tmax; }
+        else { as0 += tmin; as1 += tmax; }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      rs0 += __shfl_xor_sync(0xffffffffu, rs0, o);
+      rs1 += __shfl_xor_sync(0xffffffffu, rs1, o);
+      as0 += __shfl_xor_sync(0xffffffffu, as0, o);
+      as1 += __shfl_xor_sync(0xffffffffu, as1, o);
+    }
+    // cover leak (abstraction.py:300-309): lane d computes dimension d
+    double pa = 1.0, pl = 1.0, ph = 1.0;
+    if (lane < IMP_N) {
+      const int d = lane;
+      double mld = ml[0], mhd = mh[0];
+#pragma unroll
+      for (int e = 1; e < IMP_N; ++e)
+        if (e == d) { mld = ml[e]; mhd = mh[e]; }
+      const double lo = P.cover_lo[d], hi = P.cover_hi[d];
+      const double mu = imp_clip((lo + hi) / 2, mld, mhd);
+      const double sg = P.sigma[d];
+      pa = imp_interval_prob(sg, mu, lo, hi);
+      pl = imp_interval_prob(sg, mld, lo, hi);
+      ph = imp_interval_prob(sg, mhd, lo, hi);
+    }
+    double pmax = 1.0, pmin = 1.0;
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d) {
+      const double a = __shfl_sync(0xffffffffu, pa, d);
+      const double l = __shfl_sync(0xffffffffu, pl, d);
+      const double h = __shfl_sync(0xffffffffu, ph, d);
+      pmax = d == 0 ? a : pmax * a;
+      pmin = d == 0 ? fmin(l, h) : pmin * fmin(l, h);
+    }
+    if (lane == 0) {
+      double* raw = P.raw + r * 6;
+      raw[0] = rs0;
+      raw[1] = rs1;
+      raw[2] = as0;
+      raw[3] = as1;
+      raw[4] = fmax(0.0, 1.0 - pmax);
+      raw[5] = fmax(0.0, 1.0 - pmin);
+    }
+  }
+}
+
+
 // ---------------------------------------------------------------------------
 // Stage 3: coupled refinement, one thread per NM instance
 // ---------------------------------------------------------------------------
