@@ -350,6 +350,12 @@ def run_b200(args):
                     "note": "phase-1 iterations of the timed steps: same "
                             "algorithmic bytes over the full iteration time"},
     }
+    if traffic and "k_refine_fp64_pipe_pct" in traffic:
+        roofline["ncu_fp64_pipe_active_pct"] = traffic["k_refine_fp64_pipe_pct"]
+        roofline["note"] = ("algorithmic flops (SURVEY.md 8d) over the DFMA "
+                            "peak; bit parity keeps cephes' Horner steps as "
+                            "unfused DMUL + DADD, so the FP64 pipe (ncu) is "
+                            "busier than the algorithmic fraction shows")
     if traffic and "k_refine_dram_bytes_per_eval" in traffic:
         roofline["traffic"] = traffic["k_refine_dram_bytes_per_eval"] * \
             report.nm_evals
