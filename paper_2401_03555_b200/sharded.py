@@ -200,8 +200,8 @@ def synthesize(engine, dist, spec, mode="pessimistic", eps=1e-6, horizon=None,
 
 
 def _h2d(cfg, labels):
-    from bench import _h2d_bytes
-    return _h2d_bytes(cfg, labels)
+    from .benchutil import h2d_bytes
+    return h2d_bytes(cfg, labels)
 
 
 def bench_step(args, cfg, labels, world, rank, device):
@@ -222,7 +222,7 @@ def bench_step(args, cfg, labels, world, rank, device):
     builds, synths, sweeps, walls = [], [], [], []
     sampler = None
     if rank == 0:
-        from bench import ClockSampler
+        from .benchutil import ClockSampler
         sampler = ClockSampler(device)
     l0 = None
     ctrl_bytes = 0
