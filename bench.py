@@ -40,6 +40,9 @@ BASELINE_METRIC = ("IMDP bound entries/sec built; interval-iteration "
 DEFAULT_CONFIG = "vehicle3d"
 
 
+_JSON_FD = None   # original stdout of a sharded run (see run_b200)
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -183,6 +186,12 @@ def run_b200(args):
     sharded_path = world > 1 or os.environ.get("IMP_BENCH_FORCE_SHARDED") == "1"
     if sharded_path:
         import torch.distributed as dist
+        # NCCL writes its version banner to fd 1 when the communicator is
+        # created: route fd 1 to stderr for the whole run and keep the
+        # original stdout for the one JSON line of rank 0
+        global _JSON_FD
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     device = local
@@ -362,7 +371,9 @@ def run_sharded(args, cfg, labels, world, rank, device):
     from paper_2401_03555_b200 import sharded
     line = sharded.bench_step(args, cfg, labels, world, rank, device)
     if rank == 0 and line is not None:
-        print(json.dumps(line), flush=True)
+        sys.stdout.flush()
+        os.write(_JSON_FD if _JSON_FD is not None else 1,
+                 (json.dumps(line) + "\n").encode())
     dist.destroy_process_group()
 
 
