@@ -15,13 +15,15 @@
 // K5 uses the early-exit form of the greedy fill: with
 // P = the largest global rank such that sum_{rank<P} head < slack, a row's
 // value is  sum(l*w) + sum_{rank<P} head*w + (slack - C(<P)) * w_sorted[P].
-// P is found by a binary search over rank bits; each probe is one team-wide
-// (warp or CTA) deterministic reduction over the row's register-resident
-// entries, for both value tracks at once.  Summation order depends only on a
-// row's contents and the shared order, never on its position or shard, so
-// bitwise-identical rows give bitwise-identical values.
+// One streaming pass per row (pass A) verifies last sweep's crossing column
+// with certified float sums and walks a captured rank window when the
+// crossing moved a little; larger moves use an exact integer (2^-88 fixed
+// point) bucketed search with shared-memory atomics.  The value is always
+// built from the canonical per-lane float sums below P with a fixed team
+// tree (k_sweep, below), so it depends only on a row's contents and the
+// shared order -- never on the hint, the path taken, its position or its
+// shard: bitwise-identical rows give bitwise-identical values.
 #include <cub/device/device_radix_sort.cuh>
-#include <cuda_pipeline.h>
 
 #include <algorithm>
 #include <cstdio>
