@@ -133,6 +133,8 @@ std::string config_header(const imp_build_desc* d) {
     << "\n";
   const char* ch = getenv("IMPACT_NDTR_CHUNK");
   o << "#define IMP_NDTR_CHUNK " << (ch ? atoi(ch) : 1) << "\n";
+  const char* unr = getenv("IMPACT_NDTR_UNROLL");
+  o << "#define IMP_NDTR_UNROLL " << (unr ? atoi(unr) : 0) << "\n";
   o << "#define IMP_INST_SMEM " << inst_smem() << "\n";
   const char* batch = getenv("IMPACT_REFINE_BATCH");
   o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 4) << "\n";
