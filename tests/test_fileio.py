@@ -224,3 +224,13 @@ def test_save_matrix_vector_random(tmp_path):
     v = rng.standard_normal(1001)
     F.save_vector(tmp_path / "v.txt", v)
     assert (tmp_path / "v.txt").read_bytes() == OF.vector_bytes(v)
+
+
+@pytest.mark.gpu
+def test_save_abstraction_rejects_a_shard(tmp_path):
+    from paper_2401_03555_b200 import build_abstraction
+    g, cfg, _ = fixture("robot2d_ra_mini")
+    shard = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces,
+                              cfg.labels(), k_range=(0, 3))
+    with pytest.raises(ValueError, match="not a shard"):
+        F.save_abstraction(tmp_path, shard)
