@@ -200,6 +200,9 @@ typedef struct imp_phase_out {
   double gap;            /* final max(v1 - v0)                               */
   double ms_device;      /* device time of the loop (CUDA events)            */
   int64_t sweeps;        /* twin sweeps executed                             */
+  double ms_sweep;       /* device time of the K5 launches alone, summed over
+                          * the executed iterations (events captured into
+                          * the loop's CUDA graph around each K5 group)      */
 } imp_phase_out;
 
 /* Run one synthesis phase to termination (reference _run_phase,

@@ -82,7 +82,7 @@ class PhaseOut(ctypes.Structure):
     _fields_ = [("v0", P_dbl), ("v1", P_dbl), ("policy", P_i64),
                 ("iterations", c_i64), ("k0", c_i64), ("k1", c_i64),
                 ("fallback", c_i32), ("gap", c_dbl), ("ms_device", c_dbl),
-                ("sweeps", c_i64)]
+                ("sweeps", c_i64), ("ms_sweep", c_dbl)]
 
 
 _lib = None

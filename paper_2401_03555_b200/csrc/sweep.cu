@@ -1089,6 +1089,7 @@ int launch_sweep(SweepArgs sa, const Work& w, bool wide, int sms,
 struct Launch {
   const imp_imdp* h;
   Work* w;
+  cudaEvent_t k5_begin = nullptr, k5_end = nullptr;   // optional timing
   int sms;
   int spec, lp, u_max;
   const int64_t* fixed_dev;   // local policy or nullptr
@@ -1173,7 +1174,13 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   sa.hint = w.hint.ptr;
   sa.perm0 = w.perm[0].ptr;
   sa.perm1 = w.perm[1].ptr;
+  // (during stream capture, an External record is a real event-record
+  // node -- a plain record only orders work inside the graph)
+  if (L.k5_begin)
+    IMP_CUDA(cudaEventRecordWithFlags(L.k5_begin, s, cudaEventRecordExternal));
   const int n_sweep = launch_sweep(sa, w, w.wide, L.sms, s);
+  if (L.k5_end)
+    IMP_CUDA(cudaEventRecordWithFlags(L.k5_end, s, cudaEventRecordExternal));
   w.last_sweep = sa;
 
   ReduceArgs rd{};
@@ -1275,9 +1282,23 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     const int G = 16;
     cudaGraph_t graph;
     cudaGraphExec_t exec;
+    // K5 of every captured iteration between two events (event record
+    // nodes), read after each replay: the live K5 time of the loop
+    cudaEvent_t k5ev[2 * G];
+    for (auto& e : k5ev) IMP_CUDA(cudaEventCreate(&e));
+    struct EvGuard {
+      cudaEvent_t* e;
+      int n;
+      ~EvGuard() { for (int q = 0; q < n; ++q) cudaEventDestroy(e[q]); }
+    } evg{k5ev, 2 * G};
     IMP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     int per_graph = 0;
-    for (int g = 0; g < G; ++g) per_graph += enqueue_iteration(L, s);
+    for (int g = 0; g < G; ++g) {
+      L.k5_begin = k5ev[2 * g];
+      L.k5_end = k5ev[2 * g + 1];
+      per_graph += enqueue_iteration(L, s);
+    }
+    L.k5_begin = L.k5_end = nullptr;
     IMP_CUDA(cudaStreamEndCapture(s, &graph));
     IMP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
     struct GraphGuard {
@@ -1291,12 +1312,22 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     IMP_CUDA(cudaEventCreate(&e1));
     IMP_CUDA(cudaEventRecord(e0, s));
     Ctl hc{};
+    double ms_k5 = 0.0;
+    long long it_before = 0;
     for (;;) {
       IMP_CUDA(cudaGraphLaunch(exec, s));
       count_launches(per_graph, 2 * G);
       IMP_CUDA(cudaMemcpyAsync(&hc, w.ctl.ptr, sizeof(Ctl),
                                cudaMemcpyDeviceToHost, s));
       IMP_CUDA(cudaStreamSynchronize(s));
+      // iterations of this replay that ran (later ones exit at once)
+      const long long ran = std::min<long long>(G, hc.it - it_before);
+      for (int g = 0; g < ran; ++g) {
+        float t = 0.f;
+        IMP_CUDA(cudaEventElapsedTime(&t, k5ev[2 * g], k5ev[2 * g + 1]));
+        ms_k5 += t;
+      }
+      it_before = hc.it;
       if (hc.done) break;
     }
     IMP_CUDA(cudaEventRecord(e1, s));
@@ -1336,6 +1367,7 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     out->gap = hc.gap;
     out->ms_device = ms;
     out->sweeps = hc.it;
+    out->ms_sweep = ms_k5;
     if (hc.status != IMP_OK) {
       if (hc.status == IMP_E_CONVERGENCE)
         set_error("gap %.17g above eps=%.17g after %lld iterations", hc.gap,

@@ -69,6 +69,7 @@ class PhaseReport:
     fallback: bool
     gap: float
     ms_device: float
+    ms_sweep: float = 0.0   # K5 launches alone (live, CUDA graph events)
 
 
 def _report_k(k):
@@ -134,7 +135,7 @@ def run_phase(imdp, spec, lp_direction, u_objective, eps, horizon,
     _lib.check(st)
     return PhaseReport(ValuePair(v0, v1), pol, int(out.iterations), k0, k1,
                        bool(out.fallback), float(out.gap),
-                       float(out.ms_device))
+                       float(out.ms_device), float(out.ms_sweep))
 
 
 def bellman_step(imdp, values, lp_direction, u_objective, spec,
@@ -180,7 +181,8 @@ def _make_controller(imdp, policy, p_min, p_max, kind, mode, eps, horizon,
             "horizon": "infinite" if horizon is None else int(horizon),
             "iterations": tuple(p.iterations for p in phases),
             "fallback": tuple(p.fallback for p in phases),
-            "device_ms": tuple(p.ms_device for p in phases)}
+            "device_ms": tuple(p.ms_device for p in phases),
+            "sweep_ms": tuple(p.ms_sweep for p in phases)}
     return Controller(states=np.asarray(imdp.labels.safe).copy(),
                       coords=coords, policy=policy, inputs=inputs,
                       p_min=p_min, p_max=p_max, meta=meta)
