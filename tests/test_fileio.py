@@ -53,6 +53,7 @@ def controller_of(g, cfg, imdp):
     class _Ph:
         def __init__(self, it):
             self.iterations, self.fallback, self.ms_device = it, False, 0.0
+            self.ms_sweep = 0.0
     return _make_controller(imdp, policy, g["p_min"], g["p_max"], kind,
                             cfg.mode, cfg.eps, cfg.horizon,
                             tuple(_Ph(int(x)) for x in g["iterations"]),
