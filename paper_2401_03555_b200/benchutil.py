@@ -15,11 +15,23 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    INTERVAL_MS = 200
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
         self.path = None
+        self.skip = 0
+
+    def mark(self):
+        """Start of the timed region: samples written so far (nvidia-smi's
+        start-up, which stalls the driver for a second or more, is kept out
+        of the timed region by starting the sampler one step earlier) are
+        dropped from the summary."""
+        if self.proc is None:
+            return
+        with open(self.path) as fh:
+            self.skip = sum(1 for _ in fh)
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -28,7 +40,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
                  f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"),
+                 "-lms", str(self.INTERVAL_MS)], stdout=open(self.path, "w"),
                 stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -43,7 +55,9 @@ class ClockSampler:
             self.proc.kill()
         rows = []
         with open(self.path) as fh:
-            for line in fh:
+            for q, line in enumerate(fh):
+                if q < self.skip:
+                    continue
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) >= 8:
                     rows.append(parts)

@@ -211,11 +211,25 @@ struct NelderMead {
     done = false;
   }
 
+  // A shrink (optimize.py:140-148) moves vertex v towards the best vertex
+  // here, when v is about to be evaluated, instead of all D vertices at the
+  // shrink decision: the same arithmetic per vertex, but done on the trip
+  // every lane runs instead of in a rarely-taken branch that serialises.
   __device__ __forceinline__ void point(double* p) {
-    const bool vert = phase == NM_INIT || phase == NM_SHRINK;
+    const bool shr = phase == NM_SHRINK;
+    const bool vert = phase == NM_INIT || shr;
     const int ps = vert ? slot(v) : (phase == NM_REFLECT ? REF : CAND);
+    const int s0 = slot(0);
 #pragma unroll
-    for (int d = 0; d < D; ++d) p[d] = xs(ps, d);
+    for (int d = 0; d < D; ++d) {
+      double q = xs(ps, d);
+      if (shr) {
+        const double b = xs(s0, d);
+        q = b + 0.5 * (q - b);
+        xs(ps, d) = q;
+      }
+      p[d] = q;
+    }
   }
 
   // stable sort, termination test, centroid and reflection point
@@ -299,15 +313,7 @@ struct NelderMead {
         for (int d = 0; d < D; ++d) xs(sw, d) = xs(from, d);
         fs(sw) = use_c ? fp : fr;
         iter = true;
-      } else {
-        const int s0 = slot(0);
-#pragma unroll
-        for (int vv = 1; vv <= D; ++vv) {
-          const int sv = slot(vv);
-#pragma unroll
-          for (int d = 0; d < D; ++d)
-            xs(sv, d) = xs(s0, d) + 0.5 * (xs(sv, d) - xs(s0, d));
-        }
+      } else {   // shrink: vertices 1..D move in point()
         v = 1;
         phase = NM_SHRINK;
       }

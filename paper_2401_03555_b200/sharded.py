@@ -228,9 +228,11 @@ def bench_step(args, cfg, labels, world, rank, device):
     ctrl_bytes = 0
     for step in range(args.warmup + args.steps):
         timed = step >= args.warmup
+        if sampler and step == max(args.warmup - 1, 0):
+            sampler.start()     # nvidia-smi start-up stays out of the timing
         if timed and l0 is None:
             if sampler:
-                sampler.start()
+                sampler.mark()
             l0 = _lib.launch_count()
         dist.barrier()
         torch.cuda.synchronize()
