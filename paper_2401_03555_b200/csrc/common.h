@@ -57,7 +57,16 @@ int guarded(F&& body) {
   }
 }
 
-// Owning device buffer (cudaMalloc); movable, not copyable.
+// Device memory comes from the device's stream-ordered pool with the
+// release threshold lifted, so the multi-GB CSR of one build is reused by
+// the next instead of being unmapped and remapped (cudaFree / cudaMalloc of
+// 4-10 GB cost 0.1-3 s of host time per build).  Allocation and release stay
+// synchronous, like cudaMalloc / cudaFree: the buffer is ready on return,
+// and it is released only after the device is idle.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p);
+
+// Owning device buffer; movable, not copyable.
 template <class T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -75,10 +84,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) IMP_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    if (count) ptr = static_cast<T*>(pool_alloc(count * sizeof(T)));
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) pool_free(ptr);
     ptr = nullptr;
     n = 0;
   }

@@ -28,6 +28,36 @@ void set_error(const char* fmt, ...) {
   g_last_error = buf;
 }
 
+void* pool_alloc(size_t bytes) {
+  static std::mutex mu;
+  static bool ready[64] = {};
+  int dev = 0;
+  IMP_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && !ready[dev]) {
+      cudaMemPool_t pool;
+      IMP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t keep = ~0ull;   // never hand freed blocks back to the OS
+      IMP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold,
+                                       &keep));
+      ready[dev] = true;
+    }
+  }
+  void* p = nullptr;
+  IMP_CUDA(cudaMallocAsync(&p, bytes, cudaStreamLegacy));
+  IMP_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+  return p;
+}
+
+void pool_free(void* p) {
+  // cudaFree's implicit device synchronisation: the library's streams are
+  // non-blocking, so the buffer may still be in use by any of them
+  cudaDeviceSynchronize();
+  cudaFreeAsync(p, cudaStreamLegacy);
+  cudaStreamSynchronize(cudaStreamLegacy);
+}
+
 namespace {
 
 // Imdp.validate (reference abstraction.py:121-137) over the CSR shard.
