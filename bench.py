@@ -160,6 +160,14 @@ def cpu_sweep_baseline(n_rows, n_s, live, sample=2000, seed=7):
 
 # --- the GPU step ---------------------------------------------------------------
 
+def _overrides(args):
+    # --horizon: a finite horizon for configs whose infinite-horizon run
+    # ends, in the reference too, at the 10^6-iteration cap with a
+    # ConvergenceError (room5d); the reference suggests max(k0, k1) or any
+    # finite horizon for plain value iteration
+    return {"horizon": args.horizon} if args.horizon else {}
+
+
 def _spec_call(cfg, imdp):
     from paper_2401_03555_b200 import synthesize_reach, synthesize_safe, verify
     kw = dict(mode=cfg.mode, eps=cfg.eps, horizon=cfg.horizon,
@@ -195,7 +203,7 @@ def run_b200(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     device = local
-    cfg = benchmark(args.config)
+    cfg = benchmark(args.config, **_overrides(args))
     labels = cfg.labels()
     n_s = len(labels.safe)
     n_u = cfg.input_space.total if cfg.input_space is not None else 1
@@ -359,6 +367,7 @@ def run_b200(args):
         "config": {"workload": args.config, "rows": rows_total, "n_s": n_s,
                    "entries": entries, "nnz": nnz,
                    "spec": cfg.spec_type, "mode": cfg.mode, "eps": cfg.eps,
+                   "horizon": cfg.horizon,
                    "step": "build_abstraction + two-phase synthesis",
                    "l2": "outputs/inputs >> L2 (CSR %.1f GB)" % (
                        nnz * 20 / 1e9),
@@ -400,7 +409,7 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2401_03555_b200.config import benchmark
-    cfg = benchmark(args.config)
+    cfg = benchmark(args.config, **_overrides(args))
     labels = cfg.labels()
     n_s = len(labels.safe)
     n_u = cfg.input_space.total if cfg.input_space is not None else 1
@@ -442,6 +451,8 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--cpu-rows", type=int, default=3)
+    ap.add_argument("--horizon", type=int, default=0,
+                    help="finite horizon (0: the config's, infinite)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

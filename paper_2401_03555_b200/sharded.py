@@ -274,7 +274,7 @@ def bench_step(args, cfg, labels, world, rank, device):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.config, "rows": n_s * n_u * n_w,
-                   "n_s": n_s, "entries": entries,
+                   "n_s": n_s, "entries": entries, "horizon": cfg.horizon,
                    "step": "build_abstraction (shard) + two-phase synthesis",
                    "parallelism": f"states sharded over {world} ranks; V "
                                   "all-gathered per sweep (NCCL)"},
