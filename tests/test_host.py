@@ -183,3 +183,14 @@ class TestConfig:
         with pytest.raises(ConfigError):
             parse_config_text("[state]\nlb = 0\nub = 1\neta = 1\n"
                               "[synthesis]\nepsilon = 0\n")
+
+    def test_bench_horizon_override(self):
+        # bench.py --horizon: finite horizon for configs whose infinite-horizon
+        # run ends at the reference's iteration cap (room5d, dim14)
+        import argparse
+        import bench
+        cfg = benchmark("room5d", **bench._overrides(
+            argparse.Namespace(horizon=200)))
+        assert cfg.horizon == 200
+        assert benchmark("room5d", **bench._overrides(
+            argparse.Namespace(horizon=0))).horizon is None
