@@ -257,6 +257,22 @@ __device__ __forceinline__ Fix to_fix(double h) {
              (uint64_t)(__double_as_longlong(t2) - __double_as_longlong(M2))};
 }
 
+// Add h~ = {a, b} into a histogram bucket (two 64-bit words) with native
+// 32-bit shared-memory atomics: 64-bit shared atomicAdd is a CAS spin loop
+// on sm_100a.  The low words carry into the high words (detected from the
+// returned old value), so each 64-bit word ends as the exact sum mod 2^64:
+// a's sum stays below 2^64, b's is a two's-complement int64 -- the words
+// the scan reads are bit-identical to 64-bit adds.
+__device__ __forceinline__ void hist_add(unsigned long long* hb, Fix x) {
+  unsigned* w = reinterpret_cast<unsigned*>(hb);
+  const unsigned alo = (unsigned)x.a, ahi = (unsigned)(x.a >> 32);
+  const unsigned blo = (unsigned)x.b, bhi = (unsigned)(x.b >> 32);
+  const unsigned oa = atomicAdd(w, alo);
+  const unsigned ob = atomicAdd(w + 2, blo);
+  atomicAdd(w + 1, ahi + (oa + alo < oa ? 1u : 0u));
+  atomicAdd(w + 3, bhi + (ob + blo < ob ? 1u : 0u));
+}
+
 __device__ __forceinline__ u128 fix_value(uint64_t a, uint64_t b) {
   return (u128)(((__int128)a << 44) + (__int128)(int64_t)b);
 }
@@ -337,6 +353,15 @@ __device__ __forceinline__ void team_sum_pass_a(double* f, double* fpart,
 __device__ __forceinline__ double k5_margin(double c) {
   return fma(fabs(c), 0x1p-36, 0x1p-68);
 }
+
+// Warm-start hints, one int per (row, track): the crossing column of the
+// last sweep (HINT_COL: none, P = n) with HINT_SEARCHED set if that sweep
+// needed the bucketed search; negative: unknown (first sweep).
+constexpr int HINT_COL = 0x3fffffff;
+constexpr int HINT_SEARCHED = 0x40000000;
+#ifndef IMP_K5_SPEC
+#define IMP_K5_SPEC 0   // measured slower (profiles/r01/k5_spec_level1_experiment.log)
+#endif
 
 // Buckets per search level: CTA teams 256, warp teams 32.
 template <int TEAM>
@@ -431,19 +456,22 @@ template <int TEAM, bool WIDE>
 __device__ __noinline__ void search_levels(const SweepArgs& a, int tid,
                                            int64_t row, int64_t beg, int m,
                                            double s, SearchState& st,
-                                           unsigned long long* hist) {
+                                           unsigned long long* hist,
+                                           bool prefilled) {
   using SH = K5Shape<TEAM>;
   auto team_sync = [] {
     if constexpr (TEAM == 32) __syncwarp();
     else __syncthreads();
   };
   const u128 S = fix_ceil(s);
+  bool fill = !prefilled;   // level 1 may come filled from pass A
   while (st.act) {
     const int act = st.act;
     const int lo0 = st.lo[0], lo1 = st.lo[1];
     const int w0 = (act & 1) ? 1 << st.lg[0] : 0;
     const int w1 = (act & 2) ? 1 << st.lg[1] : 0;
     const int sh0 = max(0, st.lg[0] - SH::LOGB), sh1 = max(0, st.lg[1] - SH::LOGB);
+    if (fill) {
     for (int q = tid; q < SH::HIST; q += TEAM) hist[q] = 0ull;
     team_sync();
     for_slots<TEAM, WIDE>(a, tid, row, beg, m,
@@ -453,17 +481,11 @@ __device__ __noinline__ void search_levels(const SweepArgs& a, int tid,
           const bool in0 = d0 < (unsigned)w0, in1 = d1 < (unsigned)w1;
           if (!(in0 || in1)) return;
           const Fix x = to_fix(h);
-          if (in0) {
-            unsigned long long* hb = hist + (d0 >> sh0) * 2;
-            atomicAdd(hb, (unsigned long long)x.a);
-            atomicAdd(hb + 1, (unsigned long long)x.b);
-          }
-          if (in1) {
-            unsigned long long* hb = hist + (SH::B + (d1 >> sh1)) * 2;
-            atomicAdd(hb, (unsigned long long)x.a);
-            atomicAdd(hb + 1, (unsigned long long)x.b);
-          }
+          if (in0) hist_add(hist + (d0 >> sh0) * 2, x);
+          if (in1) hist_add(hist + (SH::B + (d1 >> sh1)) * 2, x);
         });
+    }
+    fill = true;
     team_sync();
     if (tid < 32) {   // one warp scans each active track's buckets
       const int lane = tid;
@@ -575,15 +597,28 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     const double s = a.slack[row];
     const bool zero = !(s > 0.0);   // nothing is filled: P = 0, C = 0
     bool known = zero;
+    bool flagged = false;   // the row searched last sweep
     int g0 = 0, g1 = 0;
     if (!zero && a.hint) {
       const int h0 = a.hint[2 * t], h1 = a.hint[2 * t + 1];
-      if (h0 >= -1 && h1 >= -1) {
+      if (h0 >= 0 && h1 >= 0) {
         known = true;
+        flagged = ((h0 | h1) & HINT_SEARCHED) != 0;
+        const int c0 = h0 & HINT_COL, c1 = h1 & HINT_COL;
         RankReg<WIDE> r;
-        if (h0 >= 0) { r.load(a, h0); g0 = r.r0(); } else g0 = a.n;
-        if (h1 >= 0) { r.load(a, h1); g1 = r.r1(); } else g1 = a.n;
+        if (c0 != HINT_COL) { r.load(a, c0); g0 = r.r0(); } else g0 = a.n;
+        if (c1 != HINT_COL) { r.load(a, c1); g1 = r.r1(); } else g1 = a.n;
       }
+    }
+    // rows that searched last sweep (or have no hint) will likely search
+    // again: pass A fills the first search level's histogram on the way
+    // (the same exact integer adds, so the search result is unchanged)
+    const bool spec = IMP_K5_SPEC && !zero && (!known || flagged);
+    const int shs = max(0, a.nbits - SH::LOGB);
+    if (spec) {
+      team_sync();   // the previous row's histogram adds are complete
+      for (int q = tid; q < SH::HIST; q += TEAM) hist[q] = 0ull;
+      team_sync();
     }
     // ---- pass A ----------------------------------------------------------
     // fv: lw0 lw1 | F0 F1 (sum h*w, rank < g) | C0 C1 (sum h, rank < g),
@@ -605,6 +640,11 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
           const unsigned d0 = (unsigned)(r0 - wb0), d1 = (unsigned)(r1 - wb1);
           if (d0 < 2 * W) win[d0] = h;
           if (d1 < 2 * W) win[2 * W + d1] = h;
+          if (spec) {
+            const Fix x = to_fix(h);
+            hist_add(hist + ((unsigned)r0 >> shs) * 2, x);
+            hist_add(hist + (SH::B + ((unsigned)r1 >> shs)) * 2, x);
+          }
         });
     team_sum_pass_a<TEAM>(fv, f_part, s_win[slot][par ^ 1], SH::WIN);
     int P[2] = {g0, g1};
@@ -666,7 +706,7 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
       }
       team_sync();
       if (need[0] == 2 || need[1] == 2)
-        search_levels<TEAM, WIDE>(a, tid, row, beg, m, s, st, hist);
+        search_levels<TEAM, WIDE>(a, tid, row, beg, m, s, st, hist, spec);
       // ---- pass F: the canonical float sums below the new crossings -----
       // (same per-lane order and team tree as pass A, so a row's bits do not
       // depend on which path found P)
@@ -691,9 +731,12 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
       team_sync();   // st is reused by the team's next row
     }
     if (tid == 0) {
-      if (a.hint && (need[0] | need[1])) {   // crossing columns for next sweep
-        a.hint[2 * t] = P[0] >= a.n ? -1 : __ldg(a.perm0 + P[0]);
-        a.hint[2 * t + 1] = P[1] >= a.n ? -1 : __ldg(a.perm1 + P[1]);
+      if (a.hint && (need[0] | need[1] | (int)flagged)) {
+        // crossing columns for next sweep, flagged if this row searched
+        const int fl = (need[0] == 2 || need[1] == 2) ? HINT_SEARCHED : 0;
+        a.hint[2 * t] = (P[0] >= a.n ? HINT_COL : __ldg(a.perm0 + P[0])) | fl;
+        a.hint[2 * t + 1] =
+            (P[1] >= a.n ? HINT_COL : __ldg(a.perm1 + P[1])) | fl;
       }
       a.out0[t] = row_value(fv[0], fv[2], s, fv[4], P[0], a.n, a.ws0);
       a.out1[t] = row_value(fv[1], fv[3], s, fv[5], P[1], a.n, a.ws1);
