@@ -111,6 +111,8 @@ struct imp_imdp {
   imp::DevBuf<double> lo, hi;    // nnz   (t_min, t_max of stored entries)
   imp::DevBuf<double> r_min, r_max, a_min, a_max;  // n_rows
   imp::DevBuf<double> slack;     // n_rows: max(0, 1 - sum(lower))
+  imp::DevBuf<double> hd;        // nnz: hi - lo (heads, for the sweep passes
+                                 // that read no lower bounds)
   // working set cached by host-driven (sharded) iterations
   void* sweep_cache = nullptr;
   int64_t sweep_cache_rows = -1;

@@ -158,6 +158,7 @@ struct SweepArgs {
   const int32_t* col;
   const double* lo;
   const double* hi;
+  const double* hd;         // hi - lo per stored entry (finalize_imdp)
   const double* r_min;
   const double* r_max;
   const double* a_min;
@@ -391,8 +392,11 @@ struct K5Shape {
 
 // Stream the row's slots in the canonical per-lane order -- entries
 // q = tid, tid + TEAM, ... (U loads in flight), then the two virtual slots
-// on team thread 0 -- calling f(l, h, w, rank) for each.
-template <int TEAM, bool WIDE, class Fn>
+// on team thread 0 -- calling f(l, h, w, rank) for each.  Heads come from
+// the precomputed hd = hi - lo (bit-identical to forming it here); passes
+// that need no lower bound (NEED_L false: search levels, pass F) read
+// 12 B per entry instead of 20 B, and get l = 0.
+template <int TEAM, bool WIDE, bool NEED_L = true, class Fn>
 __device__ __forceinline__ void for_slots(const SweepArgs& a, int tid,
                                           int64_t row, int64_t beg, int m,
                                           Fn&& f) {
@@ -402,7 +406,7 @@ __device__ __forceinline__ void for_slots(const SweepArgs& a, int tid,
   constexpr int U = IMP_K5_U;
   const int32_t* colp = a.col + beg;
   const double* lop = a.lo + beg;
-  const double* hip = a.hi + beg;
+  const double* hdp = a.hd + beg;
   for (int q = tid; q < m; q += U * TEAM) {
     int c[U];
     double l[U], u[U];
@@ -413,8 +417,8 @@ __device__ __forceinline__ void for_slots(const SweepArgs& a, int tid,
       l[k] = u[k] = 0.0;
       if (qq < m) {
         c[k] = __ldg(colp + qq);
-        l[k] = __ldg(lop + qq);
-        u[k] = __ldg(hip + qq);
+        if (NEED_L) l[k] = __ldg(lop + qq);
+        u[k] = __ldg(hdp + qq);
       }
     }
 #pragma unroll
@@ -422,7 +426,7 @@ __device__ __forceinline__ void for_slots(const SweepArgs& a, int tid,
       if (c[k] >= 0) {
         RankReg<WIDE> rk;
         rk.load(a, c[k]);
-        f(l[k], u[k] - l[k], __ldg(a.colw + c[k]), rk);
+        f(l[k], u[k], __ldg(a.colw + c[k]), rk);
       }
     }
   }
@@ -474,7 +478,7 @@ __device__ __noinline__ void search_levels(const SweepArgs& a, int tid,
     if (fill) {
     for (int q = tid; q < SH::HIST; q += TEAM) hist[q] = 0ull;
     team_sync();
-    for_slots<TEAM, WIDE>(a, tid, row, beg, m,
+    for_slots<TEAM, WIDE, false>(a, tid, row, beg, m,
         [&](double, double h, double2, const RankReg<WIDE>& rk) {
           const unsigned d0 = (unsigned)(rk.r0() - lo0);
           const unsigned d1 = (unsigned)(rk.r1() - lo1);
@@ -712,7 +716,7 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
       // depend on which path found P)
       const int q0 = need[0] ? st.P[0] : -1, q1 = need[1] ? st.P[1] : -1;
       double fz[4] = {0.0, 0.0, 0.0, 0.0};
-      for_slots<TEAM, WIDE>(a, tid, row, beg, m,
+      for_slots<TEAM, WIDE, false>(a, tid, row, beg, m,
           [&](double, double h, double2 w, const RankReg<WIDE>& rk) {
             if (rk.r0() < q0) { fz[0] = fma(h, w.x, fz[0]); fz[2] += h; }
             if (rk.r1() < q1) { fz[1] = fma(h, w.y, fz[1]); fz[3] += h; }
@@ -883,15 +887,20 @@ __global__ void k_control(Ctl* c) {
 // ---------------------------------------------------------------------------
 
 __global__ void k_slack(const int64_t* row_ptr, const double* lo,
-                        const double* r_min, const double* a_min,
-                        int64_t n_rows, double* slack, int* max_row) {
+                        const double* hi, const double* r_min,
+                        const double* a_min, int64_t n_rows, double* slack,
+                        double* hd, int* max_row) {
   const int lane = threadIdx.x & 31;
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = w; r < n_rows; r += nw) {
     int64_t b = row_ptr[r], e = row_ptr[r + 1];
     double acc = 0.0;
-    for (int64_t q = b + lane; q < e; q += 32) acc += lo[q];
+    for (int64_t q = b + lane; q < e; q += 32) {
+      const double l = lo[q];
+      acc += l;
+      hd[q] = hi[q] - l;   // the head K5 forms from the same two loads
+    }
     acc = warp_sum(acc);
     if (lane == 0) {
       slack[r] = fmax(0.0, 1.0 - (acc + r_min[r] + a_min[r]));
@@ -902,13 +911,14 @@ __global__ void k_slack(const int64_t* row_ptr, const double* lo,
 
 void finalize_imdp(imp_imdp* h, cudaStream_t s) {
   h->slack.alloc(std::max<int64_t>(h->n_rows, 1));
+  h->hd.alloc(std::max<int64_t>(h->nnz, 1));
   DevBuf<int> mr(1);
   IMP_CUDA(cudaMemsetAsync(mr.ptr, 0, sizeof(int), s));
   if (h->n_rows > 0) {
     int blocks = (int)std::min<int64_t>((h->n_rows * 32 + 255) / 256, 148 * 64);
-    k_slack<<<blocks, 256, 0, s>>>(h->row_ptr.ptr, h->lo.ptr, h->r_min.ptr,
-                                   h->a_min.ptr, h->n_rows, h->slack.ptr,
-                                   mr.ptr);
+    k_slack<<<blocks, 256, 0, s>>>(h->row_ptr.ptr, h->lo.ptr, h->hi.ptr,
+                                   h->r_min.ptr, h->a_min.ptr, h->n_rows,
+                                   h->slack.ptr, h->hd.ptr, mr.ptr);
     IMP_CUDA(cudaGetLastError());
   }
   int host_max = 0;
@@ -1195,6 +1205,7 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   sa.col = h->col.ptr;
   sa.lo = h->lo.ptr;
   sa.hi = h->hi.ptr;
+  sa.hd = h->hd.ptr;
   sa.r_min = h->r_min.ptr;
   sa.r_max = h->r_max.ptr;
   sa.a_min = h->a_min.ptr;
@@ -1609,6 +1620,7 @@ extern "C" int imp_row_values(imp_imdp* h, const double* weights, int32_t lp,
     sa.col = h->col.ptr;
     sa.lo = h->lo.ptr;
     sa.hi = h->hi.ptr;
+    sa.hd = h->hd.ptr;
     sa.r_min = h->r_min.ptr;
     sa.r_max = h->r_max.ptr;
     sa.a_min = h->a_min.ptr;
