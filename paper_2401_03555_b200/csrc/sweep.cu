@@ -765,6 +765,46 @@ struct ReduceArgs {
   double* stats;             // explicit-mode stats (no ctl): 5 doubles
 };
 
+// Block max of the per-state statistics (exact, order-free) into the
+// control block (or the explicit-mode stats).
+__device__ __forceinline__ void bellman_stats(const ReduceArgs& a, double d0,
+                                              double d1, double gap,
+                                              unsigned flags) {
+  Ctl* ctl = a.ctl;
+  __shared__ double sd[3][32];
+  __shared__ unsigned sf[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    d0 = fmax(d0, __shfl_down_sync(FULL, d0, o));
+    d1 = fmax(d1, __shfl_down_sync(FULL, d1, o));
+    gap = fmax(gap, __shfl_down_sync(FULL, gap, o));
+    flags |= __shfl_down_sync(FULL, flags, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { sd[0][warp] = d0; sd[1][warp] = d1; sd[2][warp] = gap; sf[warp] = flags; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      d0 = fmax(d0, sd[0][w]);
+      d1 = fmax(d1, sd[1][w]);
+      gap = fmax(gap, sd[2][w]);
+      flags |= sf[w];
+    }
+    if (ctl) {
+      atomicMax(&ctl->slot_d0, (unsigned long long)order_key(d0));
+      atomicMax(&ctl->slot_d1, (unsigned long long)order_key(d1));
+      atomicMax(&ctl->slot_gap, (unsigned long long)order_key(gap));
+      atomicOr(&ctl->slot_flags, flags);
+    } else if (a.stats) {
+      unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats);
+      atomicMax(st + 0, (unsigned long long)order_key(d0));
+      atomicMax(st + 1, (unsigned long long)order_key(d1));
+      atomicMax(st + 2, (unsigned long long)order_key(gap));
+      atomicOr(reinterpret_cast<unsigned*>(st + 3), flags);
+    }
+  }
+}
+
+
 __global__ void k_bellman(ReduceArgs a) {
   Ctl* ctl = a.ctl;
   if (ctl && ctl->done) return;
@@ -808,38 +848,76 @@ __global__ void k_bellman(ReduceArgs a) {
     if (n0 < o0 - 1e-12 || n1 > o1 + 1e-12) flags |= 1u;
     if (n0 > n1 + 1e-9) flags |= 2u;
   }
-  // block max (exact, order-free)
-  __shared__ double sd[3][32];
-  __shared__ unsigned sf[32];
-  for (int o = 16; o > 0; o >>= 1) {
-    d0 = fmax(d0, __shfl_down_sync(FULL, d0, o));
-    d1 = fmax(d1, __shfl_down_sync(FULL, d1, o));
-    gap = fmax(gap, __shfl_down_sync(FULL, gap, o));
-    flags |= __shfl_down_sync(FULL, flags, o);
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) { sd[0][warp] = d0; sd[1][warp] = d1; sd[2][warp] = gap; sf[warp] = flags; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      d0 = fmax(d0, sd[0][w]);
-      d1 = fmax(d1, sd[1][w]);
-      gap = fmax(gap, sd[2][w]);
-      flags |= sf[w];
+  bellman_stats(a, d0, d1, gap, flags);
+}
+
+// Robust Bellman reduction for many inputs: one warp per state, lanes over
+// inputs j = lane, lane + 32, ... (the min / max over disturbances per input
+// runs in the reference's order inside a lane).  The arg-best input is the
+// FIRST best (synthesis.py:97-135): lane-local scans keep the first best of
+// their subsequence, the warp keeps the best value and, on ties, the lowest
+// input -- the same pick and the same bits as the sequential scan.  A NaN
+// never replaces a best; a NaN at input 0 is the result, as sequentially.
+__global__ void k_bellman_warp(ReduceArgs a) {
+  Ctl* ctl = a.ctl;
+  if (ctl && ctl->done) return;
+  const int lane = threadIdx.x & 31;
+  const int k = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int pp = ctl ? ctl->cur : 0;
+  double d0 = 0.0, d1 = 0.0, gap = -INFINITY;
+  unsigned flags = 0;
+  if (k < a.k_count) {   // warp-uniform
+    const int U = a.n_u, nw = a.n_w;
+    const bool umax = a.u_max;
+    double b0 = 0.0, b1 = 0.0, f0 = 0.0, f1 = 0.0;
+    int p0 = INT_MAX, p1 = INT_MAX;
+    for (int j = lane; j < U; j += 32) {
+      const int64_t base = ((int64_t)k * U + j) * nw;
+      double m0 = a.val0[base], m1 = a.val1[base];
+      for (int i = 1; i < nw; ++i) {
+        double x0 = a.val0[base + i], x1 = a.val1[base + i];
+        if (umax) { m0 = fmin(m0, x0); m1 = fmin(m1, x1); }
+        else      { m0 = fmax(m0, x0); m1 = fmax(m1, x1); }
+      }
+      if (j == 0) { f0 = m0; f1 = m1; }
+      if (m0 == m0 && (p0 == INT_MAX || (umax ? m0 > b0 : m0 < b0))) { b0 = m0; p0 = j; }
+      if (m1 == m1 && (p1 == INT_MAX || (umax ? m1 > b1 : m1 < b1))) { b1 = m1; p1 = j; }
     }
-    if (ctl) {
-      atomicMax(&ctl->slot_d0, (unsigned long long)order_key(d0));
-      atomicMax(&ctl->slot_d1, (unsigned long long)order_key(d1));
-      atomicMax(&ctl->slot_gap, (unsigned long long)order_key(gap));
-      atomicOr(&ctl->slot_flags, flags);
-    } else if (a.stats) {
-      unsigned long long* st = reinterpret_cast<unsigned long long*>(a.stats);
-      atomicMax(st + 0, (unsigned long long)order_key(d0));
-      atomicMax(st + 1, (unsigned long long)order_key(d1));
-      atomicMax(st + 2, (unsigned long long)order_key(gap));
-      atomicOr(reinterpret_cast<unsigned*>(st + 3), flags);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob0 = __shfl_xor_sync(FULL, b0, o), ob1 = __shfl_xor_sync(FULL, b1, o);
+      const int op0 = __shfl_xor_sync(FULL, p0, o), op1 = __shfl_xor_sync(FULL, p1, o);
+      if (op0 != INT_MAX && (p0 == INT_MAX || (umax ? ob0 > b0 : ob0 < b0) ||
+                             (ob0 == b0 && op0 < p0))) { b0 = ob0; p0 = op0; }
+      if (op1 != INT_MAX && (p1 == INT_MAX || (umax ? ob1 > b1 : ob1 < b1) ||
+                             (ob1 == b1 && op1 < p1))) { b1 = ob1; p1 = op1; }
+    }
+    f0 = __shfl_sync(FULL, f0, 0);
+    f1 = __shfl_sync(FULL, f1, 0);
+    if (f0 != f0) { b0 = f0; p0 = 0; }
+    if (f1 != f1) b1 = f1;
+    if (lane == 0) {
+      const int g = a.k_begin + k;
+      const double o0 = a.old[0][pp][g], o1 = a.old[1][pp][g];
+      double n0 = b0, n1 = b1;
+      if (ctl && ctl->frozen0) n0 = o0;
+      if (ctl && ctl->frozen1) n1 = o1;
+      if (a.policy) a.policy[k] = p0;
+      if (ctl) {
+        a.nxt[0][pp ^ 1][g] = n0;
+        a.nxt[1][pp ^ 1][g] = n1;
+      } else {
+        a.nxt[0][0][k] = n0;
+        a.nxt[1][0][k] = n1;
+      }
+      d0 = fabs(n0 - o0);
+      d1 = fabs(n1 - o1);
+      gap = n1 - n0;
+      if (n0 < o0 - 1e-12 || n1 > o1 + 1e-12) flags |= 1u;
+      if (n0 > n1 + 1e-9) flags |= 2u;
     }
   }
+  bellman_stats(a, d0, d1, gap, flags);
 }
 
 // Termination logic of _run_phase (synthesis.py:164-205) / diagnose
@@ -1255,7 +1333,11 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   rd.u_max = L.u_max;
   rd.stats = L.stats_explicit;
   if (h->k_count > 0) {
-    k_bellman<<<(h->k_count + 255) / 256, 256, 0, s>>>(rd);
+    if (!rd.fixed && rd.n_u >= 16)
+      k_bellman_warp<<<(int)(((int64_t)h->k_count * 32 + 255) / 256), 256, 0,
+                       s>>>(rd);
+    else
+      k_bellman<<<(h->k_count + 255) / 256, 256, 0, s>>>(rd);
     IMP_CUDA(cudaGetLastError());
   }
   if (ctl) {
