@@ -256,6 +256,8 @@ def bench_step(args, cfg, labels, world, rank, device):
             walls.append((w1 - w0) * 1e3)
             ctrl_bytes = sum(np.asarray(a).nbytes for a in res[:3]
                              if a is not None)
+        if step < args.warmup + args.steps - 1:
+            del eng, imdp   # the next build reuses the pooled CSR blocks
     l1 = _lib.launch_count()
     clocks = sampler.stop() if sampler else None
     mx = torch.tensor([np.mean(builds), np.mean(synths), np.mean(walls)],
