@@ -129,9 +129,11 @@ def run_phase(engine, dist, spec, lp, u_obj, eps, horizon, max_iterations,
         n0, n1, pol, st = engine.sweep(v0, v1, spec_c, lp_c, u_max)
         st = st.clone()
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
-        d0, d1, gap, mono, brk = (float(x) for x in st.cpu().tolist())
+        # the gathers are queued before the host reads the statistics, so
+        # their launches overlap the sweep instead of following the sync
         v0 = _gather(dist, n0, n_s, world, counts, engine.zeros)
         v1 = _gather(dist, n1, n_s, world, counts, engine.zeros)
+        d0, d1, gap, mono, brk = (float(x) for x in st.cpu().tolist())
         if mono > 0:
             raise ImpactError("value iterates lost monotonicity; "
                               "abstraction bounds inconsistent")
