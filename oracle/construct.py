@@ -254,9 +254,12 @@ def row_bounds(ctx, row):
             max(0.0, 1.0 - p_hi), max(0.0, 1.0 - p_lo))
 
 
-def assemble(t_min, t_max, r_min, r_max, av_min, av_max, leak_min, leak_max):
+def assemble(t_min, t_max, r_min, r_max, av_min, av_max, leak_min, leak_max,
+             monte_carlo=False):
     """Clip, repair row sums, validate (abstraction.py:607-659, :121-137).
-    Works in place on the (rows, n_s) arrays; returns the six bound arrays."""
+    Works in place on the (rows, n_s) arrays; returns the six bound arrays.
+    Monte Carlo rows skip the hard row-sum errors and are only repaired
+    (abstraction.py:620-632, 645-650: `if not monte_carlo`)."""
     np.clip(t_min, 0.0, 1.0, out=t_min)
     np.clip(t_max, 0.0, 1.0, out=t_max)
     np.minimum(t_min, t_max, out=t_min)
@@ -267,7 +270,7 @@ def assemble(t_min, t_max, r_min, r_max, av_min, av_max, leak_min, leak_max):
     a_min = np.clip(leak_min + av_min, 0.0, 1.0)
     a_max = np.clip(leak_max + av_max, 0.0, 1.0)
     over = np.maximum(t_min.sum(axis=1) + r_min + a_min - 1.0, 0.0)
-    if (over > ROW_SUM_HARD).any():
+    if not monte_carlo and (over > ROW_SUM_HARD).any():
         r = int(np.argmax(over > ROW_SUM_HARD))
         raise AbstractionError(f"row {r}: min-side sum exceeds 1 by "
                                f"{float(over[r])!r}")
@@ -281,7 +284,7 @@ def assemble(t_min, t_max, r_min, r_max, av_min, av_max, leak_min, leak_max):
         t_min[hot] *= f[:, None]
         r_min[hot] *= f
     short = np.maximum(1.0 - (t_max.sum(axis=1) + r_max + a_max), 0.0)
-    if (short > ROW_SUM_HARD).any():
+    if not monte_carlo and (short > ROW_SUM_HARD).any():
         r = int(np.argmax(short > ROW_SUM_HARD))
         raise AbstractionError(f"row {r}: max-side sum falls short of 1 by "
                                f"{float(short[r])!r}")

@@ -116,7 +116,7 @@ def build(dyn, noise, spaces, labels, opts, rows=None):
     t_min = np.stack([x[0] for x in res])
     t_max = np.stack([x[1] for x in res])
     vec = [np.array([x[q] for x in res]) for q in range(2, 8)]
-    out = assemble(t_min, t_max, *vec)
+    out = assemble(t_min, t_max, *vec, monte_carlo=True)
     return dict(zip(("t_min", "t_max", "r_min", "r_max", "a_min", "a_max"),
                     out))
 

@@ -188,6 +188,8 @@ horizon = infinite
 }
 
 # Full-size benchmark configs sampled row-wise (BASELINE.json configs 1-5).
+# The first count is the seeded uniform draw (kept from round 1 so earlier
+# rows stay in the fixtures); STRATA adds stratified rows on top.
 SAMPLES = {
     "robot2d_reachavoid": 96,
     "vehicle3d": 12,
@@ -195,6 +197,14 @@ SAMPLES = {
     "bas7d_verify": 24,
     "dim14_verify": 8,
     "robot2d_reach": 64,
+}
+# Stratified extra rows per config: boundary states (a coordinate on the
+# grid's edge), states next to a target / avoid state, and random interior
+# states, with the input index cycling so every input appears.
+STRATA = {
+    "vehicle3d": 72,
+    "room5d": 64,
+    "bas7d_verify": 48,
 }
 
 
@@ -238,6 +248,41 @@ def _one_row(row):
     return A._compute_one_row(_CTX, row, k, j, i)
 
 
+def stratified_rows(space, labels, n_u, n_w, n, seed):
+    """n rows: a third boundary states, a third states with a target / avoid
+    neighbour (one lattice step in one dimension), the rest random; input
+    index cycling over all inputs, disturbance index random."""
+    rng = np.random.default_rng(seed)
+    counts = np.asarray(space.counts, dtype=np.int64)
+    safe = np.asarray(labels.safe, dtype=np.int64)
+    multi = np.stack(np.unravel_index(safe, tuple(counts)), axis=1)
+    edge = np.any((multi == 0) | (multi == counts - 1), axis=1)
+    special = np.zeros(space.total, dtype=bool)
+    special[np.asarray(labels.target, dtype=np.int64)] = True
+    special[np.asarray(labels.avoid, dtype=np.int64)] = True
+    near = np.zeros(len(safe), dtype=bool)
+    for d in range(len(counts)):
+        for step in (-1, 1):
+            m = multi.copy()
+            m[:, d] += step
+            ok = (m[:, d] >= 0) & (m[:, d] < counts[d])
+            flat = np.ravel_multi_index(tuple(np.clip(m, 0, counts - 1).T),
+                                        tuple(counts))
+            near |= ok & special[flat]
+    pools = [np.flatnonzero(edge), np.flatnonzero(near),
+             np.arange(len(safe))]
+    per = [n // 3, n // 3, n - 2 * (n // 3)]
+    ks = []
+    for pool, c in zip(pools, per):
+        if len(pool) == 0:
+            pool = pools[2]
+        ks.append(rng.choice(pool, size=min(c, len(pool)), replace=False))
+    ks = np.concatenate(ks)
+    js = (rng.integers(n_u) + np.arange(len(ks))) % n_u
+    iw = rng.integers(n_w, size=len(ks))
+    return (ks * n_u + js) * n_w + iw
+
+
 def make_rows(name, nsamp, workers):
     global _CTX
     cfg = load(name)
@@ -248,8 +293,12 @@ def make_rows(name, nsamp, workers):
     n_rows = len(labels.safe) * ctx.n_u * ctx.n_w
     rng = np.random.default_rng(1)
     rows = np.sort(rng.choice(n_rows, size=min(nsamp, n_rows), replace=False))
+    extra = np.zeros(0, np.int64)
+    if STRATA.get(name):
+        extra = stratified_rows(cfg.state_space, labels, ctx.n_u, ctx.n_w,
+                                STRATA[name], seed=2)
     # always include the first and last row (boundary cells)
-    rows = np.unique(np.concatenate([[0, n_rows - 1], rows]))
+    rows = np.unique(np.concatenate([[0, n_rows - 1], rows, extra]))
     _CTX = ctx
     t0 = time.time()
     with multiprocessing.get_context("fork").Pool(workers) as pool:
@@ -385,6 +434,118 @@ def make_full(name, workers, max_iter=None):
           f"synth {t_syn:.1f}s, err={out['error']}", flush=True)
 
 
+# --- full-size reference runs (controller + traces, no matrices) -----------
+
+def _lean_stack_bounds(imdp):
+    """S._stack_bounds, then t_min / t_max re-pointed at views of the stacked
+    copies: same values, one dense copy fewer (robot2d_reachavoid: 17.5 GB),
+    so the reference's own synthesis fits a 62 GB host."""
+    lower, upper = _ORIG_STACK(imdp)
+    imdp.t_min = lower[:, :imdp.n_s]
+    imdp.t_max = upper[:, :imdp.n_s]
+    return lower, upper
+
+
+_ORIG_STACK = S._stack_bounds
+
+
+def make_fullsize(name, workers, trace_iters=6, max_iter=None):
+    """The reference end to end at full size: build_abstraction (fork pool),
+    then synthesize_* / verify through its own _run_phase.  A spy on
+    bellman_step records the phase-1 V0 / V1 of the first `trace_iters`
+    iterations, every phase-1 policy's change count and gap, and the last
+    V0 (for top-2 margins).  Only vectors are stored: the abstraction itself
+    is rebuilt by the GPU in the test."""
+    cfg = load(name)
+    labels = cfg.labels()
+    spaces = (cfg.state_space, cfg.input_space, cfg.disturb_space)
+    cfg.workers = workers
+    t0 = time.time()
+    imdp = A.build_abstraction(cfg.dynamics, cfg.noise, spaces, labels,
+                               cfg.abstraction_options())
+    t_build = time.time() - t0
+    print(f"{name}: built {imdp.n_rows}x{imdp.n_s} in {t_build:.0f}s",
+          flush=True)
+    nnz = int(np.count_nonzero((imdp.t_min != 0) | (imdp.t_max != 0)))
+    row_nnz = np.count_nonzero((imdp.t_min != 0) | (imdp.t_max != 0), axis=1)
+    out = dict(config=cfg_text(name), n_s=imdp.n_s, n_u=imdp.n_u,
+               n_w=imdp.n_w, nnz=nnz, row_nnz=row_nnz.astype(np.int32),
+               r_min=imdp.r_min, r_max=imdp.r_max, a_min=imdp.a_min,
+               a_max=imdp.a_max, t_build=t_build,
+               row_sum_min=imdp.t_min.sum(axis=1),
+               row_sum_max=imdp.t_max.sum(axis=1),
+               t_max_colsum=imdp.t_max.sum(axis=0),
+               t_min_colsum=imdp.t_min.sum(axis=0))
+    tr0, tr1, trp, gaps = [], [], [], []
+    state = {"pair": None, "phase1": True, "last": None, "calls": 0}
+    orig = S.bellman_step
+
+    def spy(imdp_, values, lp_direction, u_objective, spec, fixed_policy=None,
+            bounds=None, solver=None):
+        res = orig(imdp_, values, lp_direction, u_objective, spec,
+                   fixed_policy, bounds, solver)
+        if fixed_policy is None:
+            state["calls"] += 1
+            if state["calls"] % 2 == 1:      # V0 step of an iteration
+                state["last"] = (np.array(values, copy=True), lp_direction,
+                                 u_objective, spec, solver)
+                state["v0"] = res
+            else:                             # V1 step
+                v0n, pol = state["v0"]
+                gaps.append(float(np.max(res[0] - v0n)))
+                if len(tr0) < trace_iters:
+                    tr0.append(v0n)
+                    tr1.append(res[0])
+                    trp.append(pol)
+        return res
+
+    S.bellman_step = spy
+    S._stack_bounds = _lean_stack_bounds
+    kind = cfg.spec_type
+    kw = dict(mode=cfg.mode, eps=cfg.eps, horizon=cfg.horizon)
+    if max_iter is not None:
+        kw["max_iterations"] = max_iter
+    t0 = time.time()
+    try:
+        if imdp.input_space is None:
+            ctrl = S.verify(imdp, spec="safety" if kind == "safety"
+                            else "reach", **kw)
+        elif kind == "safety":
+            ctrl = S.synthesize_safe(imdp, **kw)
+        else:
+            ctrl = S.synthesize_reach(imdp, **kw)
+        out.update(p_min=ctrl.p_min, p_max=ctrl.p_max,
+                   iterations=np.array(ctrl.meta["iterations"]),
+                   fallback=np.array(ctrl.meta["fallback"]),
+                   policy=(ctrl.policy if ctrl.policy is not None
+                           else np.zeros(0, np.int64)),
+                   error=np.array(""))
+        if ctrl.policy is not None and state["last"] is not None:
+            v0, lp, u_obj, spec, solver = state["last"]
+            d1, d2 = (1.0, 0.0) if spec == "reach" else (0.0, 1.0)
+            vals = solver.values(np.concatenate([v0, [d1, d2]]), lp)
+            per_u = vals.reshape(imdp.n_s, imdp.n_u, imdp.n_w)
+            per_u = per_u.min(axis=2) if u_obj == "max" else per_u.max(axis=2)
+            srt = np.sort(per_u, axis=1)
+            margin = (srt[:, -1] - srt[:, -2]) if u_obj == "max" \
+                else (srt[:, 1] - srt[:, 0])
+            out.update(margin=margin, per_u=per_u, v0_last=v0)
+    except ConvergenceError as exc:
+        out.update(error=np.array("ConvergenceError"),
+                   k0=np.array(-1 if exc.k0 is None else exc.k0),
+                   k1=np.array(-1 if exc.k1 is None else exc.k1))
+    finally:
+        S.bellman_step = orig
+        S._stack_bounds = _ORIG_STACK
+    out.update(t_synth=time.time() - t0, trace_v0=np.array(tr0),
+               trace_v1=np.array(tr1), trace_pol=np.array(trp),
+               gap_trace=np.array(gaps))
+    np.savez_compressed(os.path.join(OUT, f"fullsize_{name}.npz"), **out)
+    print(f"fullsize_{name}: synth {out['t_synth']:.0f}s, "
+          f"{len(gaps)} phase-1 iterations traced, err={out['error']}",
+          flush=True)
+
+
 def make_ndtr():
     from scipy.special import ndtr
     rng = np.random.default_rng(2024)
@@ -438,6 +599,14 @@ def main():
             make_rows(name, n, args.workers)
     if on("full_robot2d_reach"):
         make_full("robot2d_reach", args.workers)
+    # explicit only (hours of CPU): the reference end to end at full size
+    if "fullsize_dim14_verify" in want:
+        # phase 1 needs ~731 sweeps and phase 2 ~1.7 M (SURVEY.md finding 7):
+        # stop phase 1 at 30 iterations through the reference's own cap
+        make_fullsize("dim14_verify", args.workers, trace_iters=30,
+                      max_iter=30)
+    if "fullsize_robot2d_reachavoid" in want:
+        make_fullsize("robot2d_reachavoid", args.workers)
 
 
 if __name__ == "__main__":

@@ -70,6 +70,34 @@ avoid = (x1 <= 0.5) & (x2 >= 2.5)
 [synthesis]
 seed = 5
 """,
+    # small cells (eta << sigma) and few samples: every destination's
+    # estimate carries its own sampling error, so min-side row sums overshoot
+    # 1 by far more than 1e-6 and max-side sums fall short -- the branch the
+    # reference repairs instead of raising (abstraction.py:620-650)
+    "mc2d_fine": """
+[state]
+lb = 0 0
+ub = 1.5 1.5
+eta = 0.25 0.25
+[input]
+lb = -0.1
+ub = 0.1
+eta = 0.2
+[dynamics]
+f1 = 0.8*x1 + 0.1*x2 + u1 + 0.15
+f2 = 0.1*x1 + 0.7*x2 + 0.25
+[noise]
+type = full
+inv_cov = 16 2 2 12
+det = 188
+samples = 16
+[spec]
+type = reach-avoid
+target = (x1 >= 1.25) & (x2 >= 1.25)
+avoid = (x1 <= 0.25) & (x2 >= 1.25)
+[synthesis]
+seed = 11
+""",
 }
 
 
