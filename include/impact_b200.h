@@ -150,6 +150,13 @@ typedef struct imp_build_desc {
    * per (dimension, coordinate, input, disturbance); NULL: per row */
   const double* dim_lo;
   const double* dim_hi;
+  /* 1 (the Python default): the k_refine objective's normal CDFs are
+   * scipy's bit for bit (cephes with unfused Horner steps, IEEE quotient);
+   * 0: the fast objective -- the same cephes formula with fused Horner
+   * steps and a reciprocal-seeded quotient, within a few ulps per CDF
+   * (tests/test_construct_gpu.py).  The outer-bound tables, and with them
+   * the live sets, are bit-exact in both modes. */
+  int32_t exact;
 } imp_build_desc;
 
 /* Per-build timings (device milliseconds, CUDA events) and counters. */
@@ -160,6 +167,8 @@ typedef struct imp_build_stats {
   int64_t nm_evals;          /* objective evaluations (all NM instances)    */
   int64_t nm_lane_slots;     /* refine-loop lane slots (warp trips x 32):
                                 nm_evals / nm_lane_slots = SIMT efficiency */
+  int64_t nm_evals_shared;   /* of nm_evals: initial-simplex values a max
+                                run took from its min run (not evaluated) */
 } imp_build_stats;
 
 int imp_build(const imp_build_desc* desc, imp_imdp** out,
@@ -170,6 +179,14 @@ int imp_build(const imp_build_desc* desc, imp_imdp** out,
  * cubin_path when non-NULL (for cuobjdump).  IMP_E_JIT carries the NVRTC
  * log in imp_last_error(). */
 int imp_jit_compile(const imp_build_desc* desc, const char* cubin_path);
+
+/* Test entry: the construction module's device normal CDFs (reference
+ * scipy.special.ndtr, noise.py:14, 116-118) on n host values.  which = 0:
+ * the round-1 branch-free cephes form, 1: the form the default (exact)
+ * k_refine objective uses -- both bit-identical to scipy -- 2: the fast
+ * objective's fused form (a few ulps). */
+int imp_ndtr_eval(const imp_build_desc* desc, const double* x, double* y,
+                  int64_t n, int32_t which);
 
 /* ---------------------------------------------------------------------- */
 /* Interval iteration (reference synthesis.py:97-361)                      */

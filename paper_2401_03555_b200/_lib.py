@@ -52,7 +52,8 @@ class BuildDesc(ctypes.Structure):
                 ("k_begin", c_i32), ("k_count", c_i32),
                 ("mc", c_i32), ("mc_samples", c_i32),
                 ("mc_seed", ctypes.c_uint64), ("mc_norm", c_dbl),
-                ("inv_cov", P_dbl), ("dim_lo", P_dbl), ("dim_hi", P_dbl)]
+                ("inv_cov", P_dbl), ("dim_lo", P_dbl), ("dim_hi", P_dbl),
+                ("exact", c_i32)]
 
 
 class BuildStats(ctypes.Structure):
@@ -60,7 +61,7 @@ class BuildStats(ctypes.Structure):
                 ("ms_outer", c_dbl), ("ms_refine", c_dbl),
                 ("ms_assemble", c_dbl), ("nnz", c_i64),
                 ("nm_instances", c_i64), ("nm_evals", c_i64),
-                ("nm_lane_slots", c_i64)]
+                ("nm_lane_slots", c_i64), ("nm_evals_shared", c_i64)]
 
 
 class PhaseDesc(ctypes.Structure):
@@ -113,6 +114,8 @@ def _declare(lib):
     lib.imp_shard_sweep.argtypes = [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32,
                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]
     lib.imp_fp64_peak.argtypes = [c_i32, P_dbl]
+    lib.imp_ndtr_eval.argtypes = [ctypes.POINTER(BuildDesc), P_dbl, P_dbl,
+                                  c_i64, c_i32]
     lib.imp_jit_compile.argtypes = [ctypes.POINTER(BuildDesc),
                                     ctypes.c_char_p]
     lib.imp_export_text_rows.argtypes = [c_vp, c_i32, c_i64, c_i64,
@@ -142,7 +145,7 @@ EXPORTED = ("imp_last_error", "imp_version", "imp_device_query",
             "imp_run_phase", "imp_bellman_step", "imp_row_values",
             "imp_shard_sweep", "imp_fp64_peak", "imp_time_sweep",
             "imp_launch_count", "imp_export_text_rows",
-            "imp_format_values", "imp_simulate")
+            "imp_format_values", "imp_simulate", "imp_ndtr_eval")
 
 
 def launch_count():

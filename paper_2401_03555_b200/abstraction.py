@@ -14,6 +14,7 @@ tests do, is uploaded on first use.
 """
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass
 
@@ -251,19 +252,33 @@ class BuildReport:
     nm_lane_slots: int    # refine-loop lane slots; evals / slots = SIMT eff.
     rows: int
     entries: int          # rows * n_s: the reference's `d`
+    nm_evals_shared: int = 0   # of nm_evals: initial-simplex values reused
+
+
+def exact_default():
+    """Construction mode when build_abstraction gets exact=None: the exact
+    (scipy-identical) refinement objective unless IMPACT_EXACT=0 is set."""
+    return os.environ.get("IMPACT_EXACT", "1") not in ("", "0")
 
 
 def build_abstraction(dyn, noise, spaces, labels, opts=None,
-                      device=0, k_range=None) -> Imdp:
+                      device=0, k_range=None, exact=None) -> Imdp:
     """Construct the interval abstraction on the GPU.
 
     spaces = (state, input or None, disturbance or None), exactly as the
     reference (abstraction.py:551-599).  `k_range=(k_begin, k_count)`
     builds one shard of safe states (multi-GPU row sharding); the default
-    is all of them.
+    is all of them.  By default (`exact=True`) the refinement objective's
+    normal CDFs are scipy's bit for bit, so abstractions of dynamics without
+    x-dependent library calls are bit-identical to the reference's.
+    `exact=False` opts into the fast objective (fused Horner steps, within
+    a few ulps per CDF): 1.3-1.6x faster refinement, but a Nelder-Mead run
+    that flips on an ulp-level near-tie may stop at another point
+    (DESIGN.md section 5).  Live sets are exact either way.
     """
     state, inp, dist = spaces
     desc, keep = describe(dyn, noise, spaces, labels, opts, device, k_range)
+    desc.exact = int(exact_default() if exact is None else bool(exact))
     raw = ctypes.c_void_p()
     stats = _lib.BuildStats()
     _lib.check(_lib.load().imp_build(ctypes.byref(desc), ctypes.byref(raw),
@@ -275,17 +290,41 @@ def build_abstraction(dyn, noise, spaces, labels, opts=None,
     imdp.build_report = BuildReport(
         stats.ms_total, stats.ms_mean_ranges, stats.ms_outer,
         stats.ms_refine, stats.ms_assemble, stats.nnz, stats.nm_instances,
-        stats.nm_evals, stats.nm_lane_slots, rows, rows * desc.n_s)
+        stats.nm_evals, stats.nm_lane_slots, rows, rows * desc.n_s,
+        stats.nm_evals_shared)
     return imdp
 
 
-def jit_compile(dyn, noise, spaces, labels, opts=None, cubin_path=None):
+def jit_compile(dyn, noise, spaces, labels, opts=None, cubin_path=None,
+                exact=None):
     """NVRTC-compile the construction module for this system (no GPU
     needed); raises RuntimeError with the NVRTC log on failure."""
     desc, keep = describe(dyn, noise, spaces, labels, opts, 0, None)
+    desc.exact = int(exact_default() if exact is None else bool(exact))
     path = None if cubin_path is None else str(cubin_path).encode()
     _lib.check(_lib.load().imp_jit_compile(ctypes.byref(desc), path))
     del keep
+
+
+def device_ndtr(x, which=1, device=0):
+    """Test hook: the construction module's device normal CDFs of x
+    (which: 0 round-1 exact form, 1 the default exact objective's form,
+    2 the fast objective's), compiled for a trivial 1-D system."""
+    from .expr import DynamicsSpec, parse_expression
+    from .grid import build_space, label_states
+    sp = build_space([0.0], [1.0], [1.0])
+    dyn = DynamicsSpec((parse_expression("0.5*x1", (1, 0, 0)),), (1, 0, 0))
+    desc, keep = describe(dyn, DiagonalNormal(np.array([1.0])),
+                          (sp, None, None), label_states(sp), None, device,
+                          None)
+    desc.exact = 1
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    _lib.check(_lib.load().imp_ndtr_eval(
+        ctypes.byref(desc), _lib.ptr(x, _lib.c_dbl), _lib.ptr(y, _lib.c_dbl),
+        len(x), int(which)))
+    del keep
+    return y
 
 
 def describe(dyn, noise, spaces, labels, opts=None, device=0, k_range=None):

@@ -112,6 +112,9 @@ struct BuildParams {
   unsigned long long mc_seed;
   double mc_norm;
   const double* inv_cov;      // (N, N)
+  // destination boxes: {edges[b_d], edges[b_d + 1]} of every lattice state,
+  // (total, N), so k_refine's item setup needs no integer divisions
+  const double2* box;
 };
 
 __device__ __forceinline__ int imp_max_evals(const BuildParams& P, int dim) {
@@ -183,6 +186,7 @@ struct NelderMead {
   double lo[D], hi[D];
   double fr, tol, best;
   int phase, v, evals, kind, max_evals;
+  int pend;    // iterate() owed: 0 no, 1 insert the new worst, 2 full sort
   bool done;
 
   __device__ __forceinline__ int slot(int q) const {
@@ -208,7 +212,22 @@ struct NelderMead {
     phase = NM_INIT;
     v = 0;
     evals = 0;
+    pend = 0;
     done = false;
+  }
+
+  // The max instance of a box starts from the same simplex as its min
+  // instance (optimize.py:60-72: the starts and the cell are shared), so
+  // its initial values are the min run's, negated (the objective is
+  // prob * -1.0, _BoxProbObjective:349): no evaluations, same bits.
+  // Fi[q * S] holds the min run's values in vertex order.
+  __device__ void start_shared(const double* s, const double* Fi) {
+    start(s);
+#pragma unroll
+    for (int q = 0; q <= D; ++q) fs(q) = Fi[q * S] * -1.0;
+    v = D + 1;
+    evals = D + 1;
+    pend = 2;
   }
 
   // A shrink (optimize.py:140-148) moves vertex v towards the best vertex
@@ -232,25 +251,42 @@ struct NelderMead {
     }
   }
 
-  // stable sort, termination test, centroid and reflection point
-  __device__ void iterate() {
-    double key[D + 1];
-    int sl[D + 1];
+  // stable sort, termination test, centroid and reflection point.
+  // full: every vertex may have moved (initial simplex, shrink) -- rank all
+  // D + 1 keys.  Otherwise only the worst slot got a new value while the
+  // others stay sorted: numpy's stable argsort of [sorted prefix, new] puts
+  // the new key after every prefix key <= it, so one pass of D compares
+  // finds its rank (optimize.py:75-78).
+  __device__ void iterate(bool full) {
+    pend = 0;
+    if (full) {
+      double key[D + 1];
+      int sl[D + 1];
 #pragma unroll
-    for (int q = 0; q <= D; ++q) {
-      sl[q] = slot(q);
-      key[q] = fs(sl[q]);
+      for (int q = 0; q <= D; ++q) {
+        sl[q] = slot(q);
+        key[q] = fs(sl[q]);
+      }
+      unsigned long long nord = 0;
+#pragma unroll
+      for (int q = 0; q <= D; ++q) {
+        int rk = 0;
+#pragma unroll
+        for (int u = 0; u <= D; ++u)
+          rk += (key[u] < key[q]) || (u < q && key[u] == key[q]);
+        nord |= (unsigned long long)sl[q] << (4 * rk);
+      }
+      ord = nord;
+    } else {
+      const int sw = slot(D);
+      const double fn = fs(sw);
+      int r = 0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) r += fs(slot(q)) <= fn;
+      const unsigned long long low = (1ull << (4 * r)) - 1;
+      const unsigned long long mid = ord & ~low & ((1ull << (4 * D)) - 1);
+      ord = (ord & low) | ((unsigned long long)sw << (4 * r)) | (mid << 4);
     }
-    unsigned long long nord = 0;
-#pragma unroll
-    for (int q = 0; q <= D; ++q) {
-      int rk = 0;
-#pragma unroll
-      for (int u = 0; u <= D; ++u)
-        rk += (key[u] < key[q]) || (u < q && key[u] == key[q]);
-      nord |= (unsigned long long)sl[q] << (4 * rk);
-    }
-    ord = nord;
     const double f0 = fs(slot(0));
     const double spread = fs(slot(D)) - f0;
     if (!(spread > tol && evals < max_evals)) {
@@ -271,13 +307,15 @@ struct NelderMead {
     phase = NM_REFLECT;
   }
 
+  // consume the value of the last point(); the iterate() it may owe is left
+  // in `pend` so that a kernel can run it at one site for all its lanes
   __device__ void feed(double fp) {
-    bool iter = false;
+    bool iter = false, full = false;
     if (phase == NM_INIT || phase == NM_SHRINK) {
       fs(slot(v)) = fp;
       if (++v > D) {
         evals += phase == NM_INIT ? D + 1 : D;
-        iter = true;
+        iter = full = true;
       }
     } else if (phase == NM_REFLECT) {
       fr = fp;
@@ -318,7 +356,12 @@ struct NelderMead {
         phase = NM_SHRINK;
       }
     }
-    if (iter) iterate();
+    if (iter) pend = full ? 2 : 1;
+  }
+
+  __device__ void step(double fp) {
+    feed(fp);
+    if (pend) iterate(pend == 2);
   }
 };
 
@@ -379,7 +422,7 @@ __device__ long long imp_mean_box(const BuildParams& P, const double* K,
           imp_flag_nonfinite(P, flag_row);
           val = 0.0;
         }
-        nm.feed(val);
+        nm.step(val);
         ++ev;
       }
       best = fmin(best, nm.best);
@@ -1043,10 +1086,9 @@ __device__ void imp_load_item(const BuildParams& P, Instance& I) {
   for (int d = 0; d < IMP_N; ++d) {
     double lo = P.cover_lo[d], hi = P.cover_hi[d];
     if (flat >= 0) {
-      const int b = (flat / P.strides[d]) % P.counts[d];
-      const double* e = P.edges + P.edge_off[d];
-      lo = e[b];
-      hi = e[b + 1];
+      const double2 e = P.box[(long long)flat * IMP_N + d];
+      lo = e.x;
+      hi = e.y;
     }
     I.blo[d] = lo;
     I.bhi[d] = hi;
@@ -1084,11 +1126,9 @@ __device__ void imp_seek_instance(const BuildParams& P, long long g,
   imp_load_item(P, I);
 }
 
+// Next item (box): its min and max instances run together, start by start
+// (k_refine), so the item index advances by one and the sign restarts at 0.
 __device__ void imp_next_instance(const BuildParams& P, Instance& I) {
-  if (I.sgn == 0) {          // same box, max side
-    I.sgn = 1;
-    return;
-  }
   I.sgn = 0;
   if (++I.rel == I.nt + I.nx + 1) {
     ++I.row;
@@ -1102,10 +1142,15 @@ __device__ void imp_next_instance(const BuildParams& P, Instance& I) {
 __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
                                                     const Instance& I,
                                                     const double* x,
-                                                    const double* ndtr_tab) {
+                                                    const double* ndtr_tab,
+                                                    const double2* exp_tab) {
   // all 2N normal CDFs of one evaluation in one branch-free batch
   double arg[2 * IMP_N], cdf[2 * IMP_N], mean[IMP_N];
   imp_f_all(x, I.K, mean);
+#ifndef IMP_NDTR_CHUNK
+#define IMP_NDTR_CHUNK 1
+#endif
+#if IMP_EXACT
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) {
     const double m = mean[d];
@@ -1113,10 +1158,30 @@ __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
     arg[2 * d] = imp_div_rcp(I.bhi[d] - m, s, P.sig_rcp[d]);
     arg[2 * d + 1] = imp_div_rcp(I.blo[d] - m, s, P.sig_rcp[d]);
   }
-#ifndef IMP_NDTR_CHUNK
-#define IMP_NDTR_CHUNK 1
-#endif
+#if IMP_NDTR_LEGACY
+  (void)exp_tab;
   imp_ndtr_chunks<2 * IMP_N, IMP_NDTR_CHUNK>(arg, cdf, ndtr_tab);
+#else
+#pragma unroll 1
+  for (int j = 0; j < 2 * IMP_N; j += IMP_NDTR_CHUNK)
+    imp_ndtr_batch_x<IMP_NDTR_CHUNK>(arg + j, cdf + j, ndtr_tab, exp_tab);
+#endif
+#else
+  // (b - m) / sigma correctly rounded by an unchecked Markstein step
+  // (sigma in [2^-100, 2^100], build.cu exact_mode): the reference's args
+#pragma unroll
+  for (int d = 0; d < IMP_N; ++d) {
+    const double m = mean[d];
+    const double s = P.sig[d], y = P.sig_rcp[d];
+    const double nh = I.bhi[d] - m, nl = I.blo[d] - m;
+    const double qh = nh * y, ql = nl * y;
+    arg[2 * d] = fma(fma(-qh, s, nh), y, qh);
+    arg[2 * d + 1] = fma(fma(-ql, s, nl), y, ql);
+  }
+#pragma unroll 1
+  for (int j = 0; j < 2 * IMP_N; j += IMP_NDTR_CHUNK)
+    imp_ndtr_batch_fast<IMP_NDTR_CHUNK>(arg + j, cdf + j, ndtr_tab, exp_tab);
+#endif
   double prob = 1.0;
 #pragma unroll
   for (int d = 0; d < IMP_N; ++d) prob *= cdf[2 * d] - cdf[2 * d + 1];
@@ -1259,52 +1324,64 @@ __device__ void imp_store_instance(const BuildParams& P, const Instance& I,
   }
 }
 
-// Every thread owns a contiguous run of instances (balanced by count; NM
-// costs average out over thousands of instances per thread), found once by
-// binary search and then advanced incrementally.
+// Work is handed out in batches of consecutive items from a global counter
+// (a lane that finishes grabs the next batch, so warps stay full until the
+// pool drains; NM costs vary 8..max_evals evaluations per run).  A lane
+// runs an item's 2 x multistart Nelder-Mead runs in the order
+// (start 0, min), (start 0, max), (start 1, min), ...: the max run of a
+// start reuses the min run's initial simplex values (start_shared), and the
+// per-sign results are the minimum over starts (order-free).
 extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
     k_refine(BuildParams P) {
   extern __shared__ double smem[];
   __shared__ double2 s_ndtr[IMP_NDTR_TAB / 2];
   for (int q = threadIdx.x; q < IMP_NDTR_TAB; q += blockDim.x)
     imp_ndtr_fill_one(reinterpret_cast<double*>(s_ndtr), q);
+#if IMP_EXACT && IMP_NDTR_LEGACY
+  const double2* exp_tab = nullptr;
+#else
+  __shared__ double2 s_exp[128];
+  for (int q = threadIdx.x; q < 128; q += blockDim.x)
+    s_exp[q] = make_double2(imp_asd(imp_exp_tab[2 * q]),
+                            imp_asd(imp_exp_tab[2 * q + 1]));
+  const double2* exp_tab = s_exp;
+#endif
   __syncthreads();
   const double* ndtr_tab = reinterpret_cast<const double*>(s_ndtr);
   constexpr int S = IMP_REFINE_BLOCK;
   NelderMead<IMP_N, S> nm;
   nm.X = smem + threadIdx.x;
   nm.F = smem + (IMP_N + 4) * IMP_N * S + threadIdx.x;
+  // the min run's initial simplex values of the current start
+  double* Fi = smem + imp_nm_doubles<IMP_N>() * S + threadIdx.x;
 #if IMP_INST_SMEM
-  Instance& I = reinterpret_cast<Instance*>(smem + imp_nm_doubles<IMP_N>() * S)
-      [threadIdx.x];
+  Instance& I = reinterpret_cast<Instance*>(
+      smem + (imp_nm_doubles<IMP_N>() + IMP_N + 1) * S)[threadIdx.x];
 #else
   Instance I;
 #endif
   nm.tol = P.tol;
   nm.max_evals = imp_max_evals(P, IMP_N);
   const int ms = imp_multistart(P, IMP_N);
-  const long long total = 2 * P.n_items;
-  // dynamic batches of consecutive instances from a global counter: a lane
-  // that finishes grabs the next batch, so warps stay full until the pool
-  // drains (NM instance costs vary 8..max_evals evaluations)
-  constexpr long long B = IMP_REFINE_BATCH;
+  const long long total = P.n_items;
+  constexpr long long B = IMP_REFINE_BATCH / 2 > 0 ? IMP_REFINE_BATCH / 2 : 1;
   unsigned long long* counter = (unsigned long long*)P.evals + 2;
   long long g = (long long)atomicAdd(counter, (unsigned long long)B);
   long long g_end = min(total, g + B);
   if (g >= total) return;
-  imp_seek_instance(P, g, I);
+  imp_seek_instance(P, 2 * g, I);
   imp_source_cell(P, I.row, nm.lo, nm.hi);
   int s = 0;
-  double best = IMP_INF;
-  unsigned int ev = 0, slots = 0;   // per thread: far below 2^32
+  double best0 = IMP_INF, best1 = IMP_INF;
+  unsigned int ev = 0, shared = 0, slots = 0;   // per thread: far below 2^32
   {
     double st[IMP_N];
     imp_start_point<IMP_N>(nm.lo, nm.hi, 0, st);
     nm.start(st);
   }
-  // One objective evaluation per trip for every live lane; the restart path
-  // is a nested branch that reconverges before the next evaluation, so a
-  // warp never splits into groups evaluating the objective separately.
+  // One objective evaluation per trip for every live lane; run changes are
+  // a nested loop that reconverges before the next evaluation, so a warp
+  // never splits into groups evaluating the objective separately.
   bool live = true;
   while (__any_sync(__activemask(), live)) {
     ++slots;
@@ -1314,7 +1391,7 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
 #if IMP_MC
       double val = imp_mc_objective(P, I, p);
 #else
-      double val = imp_box_objective(P, I, p, ndtr_tab);
+      double val = imp_box_objective(P, I, p, ndtr_tab, exp_tab);
 #endif
       if (!imp_finite(val)) {
         imp_flag_nonfinite(P, I.row);
@@ -1322,10 +1399,30 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
       }
       ++ev;
       nm.feed(val);
-      if (nm.done) {
-        best = fmin(best, nm.best);
+      if (nm.pend == 2 && nm.phase == NM_INIT && I.sgn == 0) {
+#pragma unroll
+        for (int q = 0; q <= IMP_N; ++q) Fi[q * S] = nm.fs(q);
+      }
+      for (;;) {
+        if (nm.pend) nm.iterate(nm.pend == 2);   // the one iterate() site
+        if (!nm.done) break;
+        double st[IMP_N];
+        if (I.sgn == 0) {
+          best0 = fmin(best0, nm.best);
+          I.sgn = 1;
+          imp_start_point<IMP_N>(nm.lo, nm.hi, s, st);
+          nm.start_shared(st, Fi);
+          shared += IMP_N + 1;
+          continue;
+        }
+        best1 = fmin(best1, nm.best);
+        I.sgn = 0;
         if (++s == ms) {
-          imp_store_instance(P, I, best);
+          I.sgn = 0;
+          imp_store_instance(P, I, best0);
+          I.sgn = 1;
+          imp_store_instance(P, I, best1);
+          I.sgn = 0;
           bool more = ++g < g_end;
           if (more) {
             imp_next_instance(P, I);
@@ -1333,27 +1430,27 @@ extern "C" __global__ void __launch_bounds__(IMP_REFINE_BLOCK, IMP_REFINE_MINB)
             g = (long long)atomicAdd(counter, (unsigned long long)B);
             g_end = min(total, g + B);
             more = g < total;
-            if (more) imp_seek_instance(P, g, I);
+            if (more) imp_seek_instance(P, 2 * g, I);
           }
           if (!more) {
             live = false;
-          } else {
-            imp_source_cell(P, I.row, nm.lo, nm.hi);
-            s = 0;
-            best = IMP_INF;
+            break;
           }
+          imp_source_cell(P, I.row, nm.lo, nm.hi);
+          s = 0;
+          best0 = best1 = IMP_INF;
         }
-        if (live) {
-          double st[IMP_N];
-          imp_start_point<IMP_N>(nm.lo, nm.hi, s, st);
-          nm.start(st);
-        }
+        imp_start_point<IMP_N>(nm.lo, nm.hi, s, st);
+        nm.start(st);
       }
     }
     __syncwarp(__activemask());
   }
-  atomicAdd((unsigned long long*)P.evals, (unsigned long long)ev);
+  // [0] the reference's objective evaluations (performed + shared initial
+  // simplices), [1] lane slots, [3] evaluations saved by sharing
+  atomicAdd((unsigned long long*)P.evals, (unsigned long long)(ev + shared));
   atomicAdd((unsigned long long*)P.evals + 1, (unsigned long long)slots);
+  atomicAdd((unsigned long long*)P.evals + 3, (unsigned long long)shared);
 }
 
 
@@ -1456,5 +1553,33 @@ extern "C" __global__ void k_assemble(BuildParams P) {
       P.a_min[r] = amin;
       P.a_max[r] = amax;
     }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Test entry (imp_ndtr_eval): the module's device normal CDFs on n
+// arguments.  which = 0: imp_ndtr_batch (round-1 exact form), 1:
+// imp_ndtr_batch_x (the IMP_EXACT objective's), 2: imp_ndtr_batch_fast.
+// ---------------------------------------------------------------------------
+extern "C" __global__ void k_ndtr_eval(const double* x, double* y,
+                                       long long n, int which) {
+  __shared__ double2 s_ndtr[IMP_NDTR_TAB / 2];
+  __shared__ double2 s_exp[128];
+  for (int q = threadIdx.x; q < IMP_NDTR_TAB; q += blockDim.x)
+    imp_ndtr_fill_one(reinterpret_cast<double*>(s_ndtr), q);
+  for (int q = threadIdx.x; q < 128; q += blockDim.x)
+    s_exp[q] = make_double2(imp_asd(imp_exp_tab[2 * q]),
+                            imp_asd(imp_exp_tab[2 * q + 1]));
+  __syncthreads();
+  const double* tab = reinterpret_cast<const double*>(s_ndtr);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double a = x[i];
+    double r;
+    if (which == 0) imp_ndtr_batch<1>(&a, &r, tab);
+    else if (which == 1) imp_ndtr_batch_x<1>(&a, &r, tab, s_exp);
+    else imp_ndtr_batch_fast<1>(&a, &r, tab, s_exp);
+    y[i] = r;
   }
 }

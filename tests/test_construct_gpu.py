@@ -1,9 +1,23 @@
 """GPU construction vs the reference's golden abstractions (tests/golden).
 
-Parity rules: bounds within 1e-9 absolute -- bit-for-bit for
-dynamics without x-dependent library calls; live index sets
-(t_max > zero_cutoff) exact except entries whose reference t_max lies within
-1e-12 relative of the cutoff.
+Parity rules:
+  * live index sets (t_max > zero_cutoff) exact in both construction modes,
+    except entries whose reference t_max lies within 1e-12 relative of the
+    cutoff;
+  * default (exact=True) and dynamics without x-dependent library calls:
+    bit for bit;
+  * default and x-dependent trig (vehicle3d: CUDA vs numpy sin / cos): a
+    Nelder-Mead run whose comparisons flip on an ulp-level near-tie follows
+    a different path and stops elsewhere inside its own stopping tolerance
+    (optimize.py:80-83, tol = 1e-8 on the simplex spread): >= 99.9 % of
+    entries within FAST_TOL = 1e-12 and all within NM_TOL = 1e-8.
+    Observed on the 237 896 golden vehicle3d entries: 11 above 1e-12, max
+    1.0e-9; the REFERENCE against itself with its sin / cos results moved
+    one ulp: 60 above 1e-12, max 3.2e-9 (profiles/r02/row_parity_*.json,
+    ref_floor_*.json);
+  * opt-in fast objective (exact=False, CDFs within a few ulps of scipy's):
+    >= 99.9 % of entries within 1e-12 -- a flipped near-tie can also send a
+    run to another local optimum (once, 1.0e-3, on room5d_mini).
 """
 
 import numpy as np
@@ -21,7 +35,10 @@ from . import golden_io as G
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-9
+FAST_TOL = 1e-12
+NM_TOL = 1e-8
 SINGLE_CELL_PROB = 0.3829249225480262
+MODES = (True, False)    # exact, fast
 
 
 def make_dyn(texts, dims):
@@ -36,23 +53,28 @@ def all_safe(space):
 
 
 def compare_dense(got_min, got_max, ref_min, ref_max, cutoff=1e-12,
-                  trig=False):
-    """Bounds within TOL; for dynamics with x-dependent library calls
-    (CUDA vs numpy sin/cos bits steer a few Nelder-Mead paths apart) at
-    least 99% of entries within 1e-12 and all within the NM's own
-    resolution (1e-6).  Live index sets exact (near-cutoff excepted)."""
+                  trig=False, exact=True):
+    """The module docstring's rules; returns the largest deviation."""
     assert got_min.shape == ref_min.shape
+    worst = 0.0
     for got, ref in ((got_min, ref_min), (got_max, ref_max)):
         d = np.abs(got - ref)
-        if trig:
-            assert np.mean(d <= 1e-12) >= 0.99
-            assert d.max() <= 1e-6
+        worst = max(worst, float(d.max(initial=0.0)))
+        if not exact:
+            # opt-in fast objective: NM paths that flip on an ulp-level
+            # near-tie may stop at another local optimum (observed once on
+            # room5d_mini: 1.0e-3), so only the bulk is bounded
+            assert np.mean(d <= FAST_TOL) >= 0.999
+        elif trig:
+            assert np.mean(d <= FAST_TOL) >= 0.999
+            assert d.max() <= NM_TOL
         else:
-            assert d.max() <= TOL
+            assert np.array_equal(got, ref)
     live_g = got_max > cutoff
     live_r = ref_max > cutoff
     near = np.abs(ref_max - cutoff) <= 1e-12 * cutoff
     assert not np.any((live_g != live_r) & ~near)
+    return worst
 
 
 class TestKnownAnswers:
@@ -133,25 +155,33 @@ class TestKnownAnswers:
                               (sp, None, None), all_safe(sp))
 
 
+def vec_tol(trig, exact):
+    """r / a vectors: sums of entries, in block-tree order (not numpy's
+    pairwise order), so never compared bitwise."""
+    if not exact:
+        return 1e-2
+    return TOL if not trig else NM_TOL
+
+
+@pytest.mark.parametrize("exact", MODES)
 @pytest.mark.parametrize("name", G.MINIS)
-def test_golden_abstraction(name):
+def test_golden_abstraction(name, exact):
     if not G.have("full_" + name):
         pytest.skip("fixture not generated")
     g = G.load("full_" + name)
     cfg = G.config_of(g)
     imdp = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces,
-                             cfg.labels(), cfg.abstraction_options())
+                             cfg.labels(), cfg.abstraction_options(),
+                             exact=exact)
     ref_min, ref_max = G.dense(g)
     trig = has_x_transcendental(cfg.dynamics)
-    compare_dense(imdp.t_min, imdp.t_max, ref_min, ref_max, trig=trig)
+    # affine dynamics, exact: the whole construction is bit-for-bit the
+    # reference's (cephes ndtr + glibc exp restated, --fmad=false)
+    compare_dense(imdp.t_min, imdp.t_max, ref_min, ref_max, trig=trig,
+                  exact=exact)
     for key in ("r_min", "r_max", "a_min", "a_max"):
         d = np.abs(getattr(imdp, key) - g[key])
-        assert d.max() <= (1e-6 if trig else TOL), key
-    if not trig:
-        # affine dynamics: the whole construction is bit-for-bit the
-        # reference's (cephes ndtr + glibc exp restated, --fmad=false)
-        assert np.array_equal(imdp.t_min, ref_min)
-        assert np.array_equal(imdp.t_max, ref_max)
+        assert d.max() <= vec_tol(trig, exact), key
     imdp.validate()
 
 
@@ -159,10 +189,14 @@ ROW_SAMPLES = ("robot2d_reachavoid", "vehicle3d", "room5d", "bas7d_verify",
                "dim14_verify", "robot2d_reach")
 
 
+@pytest.mark.parametrize("exact", MODES)
 @pytest.mark.parametrize("name", ROW_SAMPLES)
-def test_golden_rows_full_size(name):
-    """Seeded rows of the full BASELINE configs, built as one-state shards
-    (k_range) so the test does not need the whole abstraction."""
+def test_golden_rows_full_size(name, exact):
+    """Seeded + stratified rows of the full BASELINE configs (boundary
+    states, states next to target / avoid, every input), built as
+    one-state shards (k_range) so the test does not need the whole
+    abstraction.  Trig dynamics: the >= 99.9 % rule over all sampled
+    entries together."""
     if not G.have("rows_" + name):
         pytest.skip("fixture not generated")
     g = G.load("rows_" + name)
@@ -171,11 +205,16 @@ def test_golden_rows_full_size(name):
     per_k = int(g["n_u"]) * int(g["n_w"])
     trig = has_x_transcendental(cfg.dynamics)
     ptr, col, lo, hi = g["ptr"], g["col"], g["lo"], g["hi"]
+    got_all, ref_all = [], []
+    built = {}
     for q, row in enumerate(g["rows"]):
         k, rel = divmod(int(row), per_k)
-        im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels,
-                               cfg.abstraction_options(), k_range=(k, 1))
-        sp, scol, slo, shi, r0, r1, a0, a1 = im.csr()
+        if k not in built:
+            built = {k: build_abstraction(
+                cfg.dynamics, cfg.noise, cfg.spaces, labels,
+                cfg.abstraction_options(), k_range=(k, 1),
+                exact=exact).csr()}
+        sp, scol, slo, shi, r0, r1, a0, a1 = built[k]
         got_min = np.zeros(int(g["n_s"]))
         got_max = np.zeros_like(got_min)
         b, e = sp[rel], sp[rel + 1]
@@ -186,11 +225,14 @@ def test_golden_rows_full_size(name):
         rb, re_ = ptr[q], ptr[q + 1]
         ref_min[col[rb:re_]] = lo[rb:re_]
         ref_max[col[rb:re_]] = hi[rb:re_]
-        compare_dense(got_min[None], got_max[None], ref_min[None],
-                      ref_max[None], trig=trig)
+        got_all.append(np.stack([got_min, got_max]))
+        ref_all.append(np.stack([ref_min, ref_max]))
         for key, got in (("r_min", r0), ("r_max", r1), ("a_min", a0),
                          ("a_max", a1)):
-            assert abs(got[rel] - g[key][q]) <= (1e-6 if trig else TOL), key
+            assert abs(got[rel] - g[key][q]) <= vec_tol(trig, exact), key
+    got_all, ref_all = np.stack(got_all), np.stack(ref_all)
+    compare_dense(got_all[:, 0], got_all[:, 1], ref_all[:, 0], ref_all[:, 1],
+                  trig=trig, exact=exact)
 
 
 def test_golden_robot2d_reach_end_to_end():
@@ -201,7 +243,8 @@ def test_golden_robot2d_reach_end_to_end():
     g = G.load("full_robot2d_reach")
     cfg = G.config_of(g)
     imdp = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces,
-                             cfg.labels(), cfg.abstraction_options())
+                             cfg.labels(), cfg.abstraction_options(),
+                             exact=True)
     ref_min, ref_max = G.dense(g)
     assert np.array_equal(imdp.t_min, ref_min)
     assert np.array_equal(imdp.t_max, ref_max)
@@ -218,3 +261,30 @@ def test_golden_robot2d_reach_end_to_end():
     per_u = g["per_u"]
     assert np.all(np.abs(per_u[k, c.policy[k]] - per_u[k, g["policy"][k]])
                   <= 1e-12)
+
+
+@pytest.mark.parametrize("which", (0, 1, 2))
+def test_device_ndtr_forms_vs_scipy(which):
+    """The k_refine objective's device CDFs on the 104 k scipy golden
+    samples (noise.py:116-118): the exact forms (0: round 1, 1: the default
+    objective's integer-classified / inline-quotient form) bit for bit;
+    the fast fused form (2) within 16 ulps relative and 4.5e-16 absolute
+    (measured: <= 12 ulps, worst next to cephes' erf / erfc switch where
+    1 - erf cancels; profiles/r02/ndtr_fast_err.txt)."""
+    from paper_2401_03555_b200.abstraction import device_ndtr
+    g = G.load("ndtr")
+    got = device_ndtr(g["x"], which)
+    want = g["y"]
+    if which < 2:
+        assert np.array_equal(got, want, equal_nan=True)
+    else:
+        # the fused form stands in P / Q for cephes' R / S at |x| >= 8 sqrt2
+        # (CDF 1 exactly, or below 1e-29): absolute agreement there
+        x = g["x"]
+        fin = np.isfinite(x)
+        err = np.abs(got[fin] - want[fin])
+        core = np.abs(x[fin]) < 8 * np.sqrt(2)
+        assert np.all(err[core] <= 16 * np.spacing(np.abs(want[fin][core])))
+        assert np.all(err[core] <= 4.5e-16)
+        assert np.all(err[~core] <= 1e-28)
+        assert np.array_equal(got[~fin], want[~fin], equal_nan=True)

@@ -198,7 +198,7 @@ def test_gpu_built_abstraction_exports_reference_t_bytes(tmp_path, name):
     from paper_2401_03555_b200 import build_abstraction
     g, cfg, _ = fixture(name)
     im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
-                           cfg.abstraction_options())
+                           cfg.abstraction_options(), exact=True)
     F.save_abstraction(tmp_path, im)
     want = digests()[name]
     got = _dir_digests(tmp_path)

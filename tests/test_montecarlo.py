@@ -24,7 +24,12 @@ TOL = 1e-12
 KEYS = ("t_min", "t_max", "r_min", "r_max", "a_min", "a_max")
 
 
-NAMES = ("mc2d_full", "mc2d_custom")
+NAMES = ("mc2d_full", "mc2d_custom", "mc2d_fine")
+# mc2d_fine: small cells and 16 samples, so per-destination sampling error
+# pushes min-side row sums past 1 + 1e-6 -- repaired, never an error, for
+# Monte Carlo rows (abstraction.py:620-650)
+ORACLE_ROWS = {"mc2d_full": [0, 9, 27], "mc2d_custom": [0, 9, 27],
+               "mc2d_fine": [0, 41]}
 
 
 def fixture(name="mc2d_full"):
@@ -35,7 +40,7 @@ def fixture(name="mc2d_full"):
 @pytest.mark.parametrize("name", NAMES)
 def test_oracle_rows_bitwise_vs_reference(name):
     g, cfg = fixture(name)
-    rows = [0, 9, 27]
+    rows = ORACLE_ROWS[name]
     out = OM.build(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
                    cfg.abstraction_options(), rows=rows)
     for k in KEYS:
@@ -69,6 +74,23 @@ def test_gpu_monte_carlo_synthesis_matches_oracle(name):
     assert tuple(c.meta["iterations"]) == tuple(want["iterations"])
     assert np.max(np.abs(c.p_min - want["p_min"])) <= 1e-9
     assert np.max(np.abs(c.p_max - want["p_max"])) <= 1e-9
+
+
+def test_fine_fixture_exercises_the_repair_branch():
+    """The reference built mc2d_fine although raw min-side sums exceed
+    1 + 1e-6 (the closed-form hard error): recompute the raw sums of two
+    rows with the oracle and check the repair branch was needed."""
+    g, cfg = fixture("mc2d_fine")
+    ctx = OM.make_context(cfg.dynamics, OM._Sigma(2), cfg.spaces,
+                          cfg.labels(), cfg.abstraction_options())
+    over = 0.0
+    for row in (0, 41):
+        t_min, _, r_min, _, av_min, _, lk_min, _ = OM.row_bounds(
+            ctx, cfg.noise, cfg.abstraction_options().mc_seed, row)
+        s = np.sum(np.clip(t_min, 0, 1)) + min(max(r_min, 0), 1) + \
+            min(max(lk_min + av_min, 0), 1)
+        over = max(over, s - 1.0)
+    assert over > 1e-6
 
 
 @pytest.mark.gpu

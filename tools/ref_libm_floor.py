@@ -1,13 +1,20 @@
-"""The reference against itself with a different libm: how far do the
-reference's own vehicle3d bounds move when its dynamics' sin / cos / tan /
-atan come from glibc's scalar libm (Python `math`) instead of numpy's SIMD
-loops?  Both are faithful (<= 1 ulp) implementations, so the spread between
-the two runs is the reference's own reproducibility floor for x-dependent
-trigonometric dynamics -- the yardstick for the GPU (CUDA libm) deviations
-in tools/row_parity_report.py.
+"""The reference against itself under one-ulp perturbations: how far do the
+reference's own vehicle3d bounds move when
+
+  mode libm:  its dynamics' sin / cos / tan / atan come from Python's
+              `math` (glibc scalar) instead of numpy's loops,
+  mode trig:  every sin / cos / tan / atan result is moved up one ulp
+              (np.nextafter) -- a different faithful libm,
+  mode ndtr:  every scipy ndtr result is moved up one ulp -- a different
+              faithful normal CDF (the GPU's fast objective is within a few
+              ulps of scipy's)?
+
+The spread between such runs and the golden rows is the reference's own
+reproducibility floor for these rows -- the yardstick for the GPU
+deviations in tools/row_parity_report.py.
 
 TEST / MEASUREMENT INFRASTRUCTURE ONLY (imports /root/reference).
-Usage: python tools/ref_libm_floor.py [workers] > profiles/r02/ref_libm_floor_vehicle3d.json
+Usage: python tools/ref_libm_floor.py MODE [workers] > profiles/r02/ref_floor_MODE_vehicle3d.json
 """
 import json
 import math
@@ -33,9 +40,24 @@ def _scalar(fn):
     return lambda x: np.asarray(uf(x), dtype=float)
 
 
-E._FUNCS.update({"sin": (_scalar(math.sin), 1), "cos": (_scalar(math.cos), 1),
-                 "tan": (_scalar(math.tan), 1),
-                 "atan": (_scalar(math.atan), 1)})
+def _up(fn):
+    return lambda x: np.nextafter(fn(x), np.inf)
+
+
+MODE = sys.argv[1] if len(sys.argv) > 1 else "libm"
+if MODE == "libm":
+    E._FUNCS.update({"sin": (_scalar(math.sin), 1),
+                     "cos": (_scalar(math.cos), 1),
+                     "tan": (_scalar(math.tan), 1),
+                     "atan": (_scalar(math.atan), 1)})
+elif MODE == "trig":
+    E._FUNCS.update({k: (_up(E._FUNCS[k][0]), 1)
+                     for k in ("sin", "cos", "tan", "atan")})
+elif MODE == "ndtr":
+    from impact import noise as N
+    N.ndtr = _up(N.ndtr)
+else:
+    raise SystemExit(f"unknown mode {MODE}")
 
 _CTX = None
 
@@ -47,7 +69,7 @@ def _row(row):
 
 def main():
     global _CTX
-    workers = int(sys.argv[1]) if len(sys.argv) > 1 else os.cpu_count()
+    workers = int(sys.argv[2]) if len(sys.argv) > 2 else os.cpu_count()
     g = G.load("rows_vehicle3d")
     path = "/tmp/ref_libm_vehicle3d.cfg"
     with open(path, "w") as fh:
@@ -60,7 +82,7 @@ def main():
     with multiprocessing.get_context("fork").Pool(workers) as pool:
         res = pool.map(_row, rows, chunksize=1)
     n = int(g["n_s"])
-    out = dict(rows=len(rows), entries=0, bitwise_rows=0, n_gt_1e12=0,
+    out = dict(mode=MODE, rows=len(rows), entries=0, bitwise_rows=0, n_gt_1e12=0,
                n_gt_1e9=0, max_abs=0.0, per_row=[])
     for q, (row, r) in enumerate(zip(rows, res)):
         rm, rx = np.zeros(n), np.zeros(n)
