@@ -23,6 +23,7 @@
 // tree (k_sweep, below), so it depends only on a row's contents and the
 // shared order -- never on the hint, the path taken, its position or its
 // shard: bitwise-identical rows give bitwise-identical values.
+#include <type_traits>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -237,8 +238,8 @@ __device__ __forceinline__ double row_value(double lw, double f, double s,
 // bucketed search with shared-memory atomics.
 // h~ is held as h~ * 2^88 = A * 2^44 + B (A = RN(h * 2^44) >= 0, B the
 // signed remainder, |B| <= 2^43), obtained with two magic-number roundings
-// in FP64 (no integer shifting).  Partial sums of A and of B over <= 2^14
-// slots stay below 2^59 in magnitude: plain 64-bit adds, no carries.
+// in FP64 (no integer shifting).  Partial sums of A and of B over < 2^20
+// slots stay below 2^64 / 2^63 in magnitude: plain 64-bit adds, no carries.
 // ---------------------------------------------------------------------------
 
 typedef unsigned __int128 u128;
@@ -344,15 +345,52 @@ __device__ __forceinline__ void team_sum_pass_a(double* f, double* fpart,
   }
 }
 
-// Certified float decisions.  The canonical float sum Cf of <= 2^14 + 2
-// heads (each in [0, 1]) is within m * 2^-53 * Cf of the true sum, which is
-// within 2^-75 of the exact fixed-point sum C~ -- so |Cf - C~| < margin(Cf)
-// and a comparison of Cf against s that clears the margin decides the exact
-// comparison the search would make.  Anything closer is left to the exact
-// search.  (Window walks add < 2^7 more float adds: the 2^-36 slope covers
-// them.)
-__device__ __forceinline__ double k5_margin(double c) {
-  return fma(fabs(c), 0x1p-36, 0x1p-68);
+// Exact sums.  Besides the crossing's C(<q) = sum h~, the filled part of
+// the value, F(<q) = sum_{rank<q} h*w, is also summed exactly: each product
+// is rounded to the 2^-88 grid once, (h w)~ (h, w in [0, 1]; error <= 2^-89
+// per slot, < 2^-68 per row), and summed as an integer.  Integer sums do not
+// depend on order, so F and C at any rank follow from F and C at another by
+// adding or removing the slots in between -- a crossing that moved inside
+// the captured window needs no second pass over the row, and the value
+// lw + F(<P) + (s - C(<P)) w_sorted[P] is a pure function of (row, weights)
+// whichever path found P.
+__device__ __forceinline__ void fix_add(Fix& s, Fix x) { s.a += x.a; s.b += x.b; }
+__device__ __forceinline__ void fix_sub(Fix& s, Fix x) { s.a -= x.a; s.b -= x.b; }
+__device__ __forceinline__ u128 fixv(Fix x) { return fix_value(x.a, x.b); }
+
+// deterministic double of an exact non-negative sum (two roundings)
+__device__ __forceinline__ double fix_double(u128 v) {
+  return fma((double)(uint64_t)(v >> 64), 0x1p-24,
+             (double)(uint64_t)v * 0x1p-88);
+}
+
+__device__ __forceinline__ Fix warp_sum_fix(Fix x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    x.a += __shfl_xor_sync(FULL, x.a, o);
+    x.b += __shfl_xor_sync(FULL, x.b, o);
+  }
+  return x;
+}
+
+// Team sums of K exact values (any order: integers)
+template <int TEAM, int K>
+__device__ __forceinline__ void team_sum_fix(Fix* v, Fix* part) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum_fix(v[k]);
+  if constexpr (TEAM > 32) {
+    constexpr int NW = TEAM / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) part[k * NW + warp] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      v[k] = warp_sum_fix(lane < NW ? part[k * NW + lane] : Fix{0, 0});
+    __syncthreads();
+  }
 }
 
 // Warm-start hints, one int per (row, track): the crossing column of the
@@ -360,9 +398,6 @@ __device__ __forceinline__ double k5_margin(double c) {
 // needed the bucketed search; negative: unknown (first sweep).
 constexpr int HINT_COL = 0x3fffffff;
 constexpr int HINT_SEARCHED = 0x40000000;
-#ifndef IMP_K5_SPEC
-#define IMP_K5_SPEC 0   // measured slower (profiles/r01/k5_spec_level1_experiment.log)
-#endif
 
 // Buckets per search level: CTA teams 256, warp teams 32.
 template <int TEAM>
@@ -377,9 +412,9 @@ struct K5Shape {
   // {a, b}, search broadcast
   static constexpr int F_PART = 6 * NW;
   static constexpr int HIST = 2 * B * 2;
-  // pass A captures h~ of the slots with rank in [g - W, g + W) per track,
-  // so a crossing that moved by < W ranks is resolved exactly in registers
-  // / shared memory without a search (only the float sum F needs a pass)
+  // pass A captures {h, w} of the slots with rank in [g - W, g + W) per
+  // track, so a crossing that moved by < W ranks is resolved exactly from
+  // shared memory, with no further pass over the row
 #ifndef IMP_K5_WWARP
 #define IMP_K5_WWARP 32
 #endif
@@ -387,14 +422,14 @@ struct K5Shape {
 #define IMP_K5_WCTA 128
 #endif
   static constexpr int W = TEAM > 32 ? IMP_K5_WCTA : IMP_K5_WWARP;
-  static constexpr int WIN = 2 * 2 * W;   // [track][slot] heads
+  static constexpr int WIN = 2 * 2 * W;   // [track][slot] {h, w}
 };
 
 // Stream the row's slots in the canonical per-lane order -- entries
 // q = tid, tid + TEAM, ... (U loads in flight), then the two virtual slots
 // on team thread 0 -- calling f(l, h, w, rank) for each.  Heads come from
 // the precomputed hd = hi - lo (bit-identical to forming it here); passes
-// that need no lower bound (NEED_L false: search levels, pass F) read
+// that need no lower bound (NEED_L false: search levels, the F pass) read
 // 12 B per entry instead of 20 B, and get l = 0.
 template <int TEAM, bool WIDE, bool NEED_L = true, class Fn>
 __device__ __forceinline__ void for_slots(const SweepArgs& a, int tid,
@@ -547,29 +582,48 @@ __device__ __noinline__ void search_levels(const SweepArgs& a, int tid,
 
 // K5: twin greedy-LP values of one class of phase rows, one row per team
 // (warp or CTA).  Value of a row for one track:
-//   val = sum l*w + [ sum_{rank<P} h*w + (s - C(<P)) * w_sorted[P] ]
-// with the float sums in the canonical per-lane order + fixed team tree,
-// and C / P exact (above).
+//   val = sum l*w + F(<P) + (s - C(<P)) * w_sorted[P]
+// with sum l*w a float sum in the canonical per-lane order + fixed team
+// tree, and P, C(<P) = sum h~, F(<P) = sum (h w)~ exact (above).
 //   pass A   one read of the row: sum l*w, and at g = the rank of last
-//            sweep's crossing column: C(<g), C(<g+1), sum_{rank<g} h*w.
-//            C(<g) < s <= C(<g+1) proves P = g -> done (most rows).
+//            sweep's crossing column: C(<g), F(<g), plus {h, w} of the
+//            slots ranked within W of g.
+//   walk     one warp: P and C, F at P by exact prefix sums over the window
+//            (most rows: the crossing moves by less than W ranks).
 //   search   otherwise, per level one pass with a shared-memory histogram
 //            of exact head sums over B rank buckets of the current range;
 //            a warp scan picks the bucket where the cumulative sum reaches
-//            s; the range shrinks by B per level (2-4 levels), to one rank.
-//   pass F   sum_{rank<P} h*w for the searched tracks (same order/tree as A).
+//            s; the range shrinks by B per level (2-4 levels), to one rank;
+//            then one pass for F(<P).
 // The result does not depend on the hint, on which path settled the row,
 // or on the row's position / shard: bitwise-identical rows give
 // bitwise-identical values.
 #ifndef IMP_K5_TPSM
 #define IMP_K5_TPSM 1024   // resident threads per SM the register cap targets
 #endif
+// Certified float decisions.  The canonical float sum Cf of <= 2^14 + 2
+// heads (warp teams: <= 514) (each in [0, 1]) is within m * 2^-53 * Cf of the true sum, which is
+// within 2^-75 of the exact fixed-point sum C~ -- so |Cf - C~| < margin(Cf)
+// and a comparison of Cf against s that clears the margin decides the exact
+// comparison the search would make.  Anything closer is left to the exact
+// search.  (Window walks add < 2^7 more float adds: the 2^-36 slope covers
+// them.)
+__device__ __forceinline__ double k5_margin(double c) {
+  return fma(fabs(c), 0x1p-36, 0x1p-68);
+}
+
+// ---------------------------------------------------------------------------
+// K5 for warp teams (rows of <= 512 stored entries): the round-1 form --
+// float sums in the canonical per-lane order with certified decisions, a
+// float window walk, and one more pass for the canonical float sums when
+// the crossing moved.  For short rows its per-row work is lighter than the
+// exact sums' (measured: robot2d_reachavoid 501 vs 322 phase-1 sweeps/s);
+// the class of a row is a function of its length alone, so either form is
+// position independent.
+// ---------------------------------------------------------------------------
 template <int TEAM, bool WIDE>
-__global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
-                                  (TEAM == 32 ? 256 : TEAM) < IMP_K5_TPSM
-                                      ? IMP_K5_TPSM / (TEAM == 32 ? 256 : TEAM)
-                                      : 1)
-    k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(256, IMP_K5_TPSM / 256)
+    k_sweep_warp(SweepArgs a) {
   if (a.ctl && a.ctl->done) return;
   using SH = K5Shape<TEAM>;
   constexpr int TEAMS_PER_BLOCK = TEAM == 32 ? 8 : 1;
@@ -617,7 +671,7 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     // rows that searched last sweep (or have no hint) will likely search
     // again: pass A fills the first search level's histogram on the way
     // (the same exact integer adds, so the search result is unchanged)
-    const bool spec = IMP_K5_SPEC && !zero && (!known || flagged);
+    const bool spec = false;
     const int shs = max(0, a.nbits - SH::LOGB);
     if (spec) {
       team_sync();   // the previous row's histogram adds are complete
@@ -745,6 +799,276 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
       a.out0[t] = row_value(fv[0], fv[2], s, fv[4], P[0], a.n, a.ws0);
       a.out1[t] = row_value(fv[1], fv[3], s, fv[5], P[1], a.n, a.ws1);
     }
+  }
+}
+
+
+
+// P, C(<P), F(<P) of one track from the window around g (one warp, all
+// lanes).  Returns false when the crossing lies W or more ranks away (the
+// caller searches).  C, F hold the exact sums at g on entry and at P on a
+// settled return; p holds g on entry and P on return.
+template <int W>
+__device__ __forceinline__ bool walk_track(bool zero, bool known, double s,
+                                           int n, int lane,
+                                           const double2* wt, Fix& C, Fix& F,
+                                           int& p) {
+  if (zero) return true;
+  if (!known) return false;
+  const u128 S = fix_ceil(s);
+  const int g = p;
+  if (fixv(C) < S) {                  // walk up: P = max{q: C(<q) < S}
+    if (g >= n) return true;          // P = n, sums unchanged
+    {                                 // common case: P = g
+      const Fix h0 = to_fix(wt[W].x);
+      if (fixv(C) + fixv(h0) >= S) return true;
+    }
+    for (int base = 0; base < W; base += 32) {
+      const int q = g + base + lane;
+      const double2 e = wt[W + base + lane];
+      const Fix hx = to_fix(e.x), fx = to_fix(e.x * e.y);
+      Fix ih = hx, ifx = fx;          // inclusive prefix over lanes
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t ya = __shfl_up_sync(FULL, ih.a, d);
+        const uint64_t yb = __shfl_up_sync(FULL, ih.b, d);
+        const uint64_t za = __shfl_up_sync(FULL, ifx.a, d);
+        const uint64_t zb = __shfl_up_sync(FULL, ifx.b, d);
+        if (lane >= d) { ih.a += ya; ih.b += yb; ifx.a += za; ifx.b += zb; }
+      }
+      // C(<q + 1) = C + ih: the crossing is the first lane reaching S
+      const unsigned hit = __ballot_sync(FULL, q < n && fixv(C) + fixv(ih) >= S);
+      const unsigned end = __ballot_sync(FULL, q >= n);
+      int L = -1;
+      if (hit) {
+        L = __ffs(hit) - 1;           // sums below q = exclusive prefix
+        p = g + base + L;
+      } else if (end) {
+        L = __ffs(end) - 1;           // no crossing before rank n
+        p = n;
+      }
+      if (L >= 0) {
+        const Fix eh{ih.a - hx.a, ih.b - hx.b}, ef{ifx.a - fx.a, ifx.b - fx.b};
+        fix_add(C, Fix{__shfl_sync(FULL, eh.a, L), __shfl_sync(FULL, eh.b, L)});
+        fix_add(F, Fix{__shfl_sync(FULL, ef.a, L), __shfl_sync(FULL, ef.b, L)});
+        return true;
+      }
+      fix_add(C, Fix{__shfl_sync(FULL, ih.a, 31), __shfl_sync(FULL, ih.b, 31)});
+      fix_add(F, Fix{__shfl_sync(FULL, ifx.a, 31), __shfl_sync(FULL, ifx.b, 31)});
+    }
+    return false;
+  }
+  {                                   // common case: P = g - 1
+    const double2 e = wt[W - 1];
+    const Fix h1 = to_fix(e.x);
+    if (fixv(C) - fixv(h1) < S) {
+      fix_sub(C, h1);
+      fix_sub(F, to_fix(e.x * e.y));
+      p = g - 1;
+      return true;
+    }
+  }
+  for (int base = 0; base < W; base += 32) {   // walk down from g - 1
+    const int q = g - 1 - base - lane;
+    const double2 e = wt[W - 1 - base - lane];
+    const Fix hx = to_fix(e.x), fx = to_fix(e.x * e.y);
+    Fix ih = hx, ifx = fx;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t ya = __shfl_up_sync(FULL, ih.a, d);
+      const uint64_t yb = __shfl_up_sync(FULL, ih.b, d);
+      const uint64_t za = __shfl_up_sync(FULL, ifx.a, d);
+      const uint64_t zb = __shfl_up_sync(FULL, ifx.b, d);
+      if (lane >= d) { ih.a += ya; ih.b += yb; ifx.a += za; ifx.b += zb; }
+    }
+    // C(<q) = C - ih (q >= 0; C(<0) = 0 < S always)
+    const unsigned hit = __ballot_sync(FULL, q >= 0 && fixv(C) - fixv(ih) < S);
+    const int L = hit ? __ffs(hit) - 1 : 31;
+    fix_sub(C, Fix{__shfl_sync(FULL, ih.a, L), __shfl_sync(FULL, ih.b, L)});
+    fix_sub(F, Fix{__shfl_sync(FULL, ifx.a, L), __shfl_sync(FULL, ifx.b, L)});
+    if (hit) {
+      p = g - 1 - base - L;
+      return true;
+    }
+  }
+  return false;
+}
+
+template <int TEAM, bool WIDE>
+__global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
+                                  (TEAM == 32 ? 256 : TEAM) < IMP_K5_TPSM
+                                      ? IMP_K5_TPSM / (TEAM == 32 ? 256 : TEAM)
+                                      : 1)
+    k_sweep(SweepArgs a) {
+  if (a.ctl && a.ctl->done) return;
+  using SH = K5Shape<TEAM>;
+  constexpr int TEAMS_PER_BLOCK = TEAM == 32 ? 8 : 1;
+  constexpr int W = SH::W;
+  __shared__ double f_part[SH::F_PART];
+  __shared__ Fix x_part[4 * SH::NW];
+  __shared__ unsigned long long hist_all[TEAMS_PER_BLOCK][SH::HIST];
+  __shared__ SearchState s_st[TEAMS_PER_BLOCK];
+  __shared__ double2 s_win[TEAMS_PER_BLOCK][2][SH::WIN];   // row parity
+  __shared__ double s_lw[TEAMS_PER_BLOCK][2];
+  __shared__ Fix s_x[TEAMS_PER_BLOCK][4];
+  __shared__ int s_need[TEAMS_PER_BLOCK][2];
+  const int tid = TEAM == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  const int slot = TEAM == 32 ? (threadIdx.x >> 5) : 0;
+  unsigned long long* hist = hist_all[slot];
+  const int64_t team0 = TEAM == 32
+      ? (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)
+      : (int64_t)blockIdx.x;
+  const int64_t nteams = TEAM == 32
+      ? (int64_t)gridDim.x * (blockDim.x >> 5) : (int64_t)gridDim.x;
+  auto team_sync = [] {
+    if constexpr (TEAM == 32) __syncwarp();
+    else __syncthreads();
+  };
+  for (int q = tid; q < 2 * SH::WIN; q += TEAM)
+    (&s_win[slot][0][0])[q] = make_double2(0.0, 0.0);
+  team_sync();
+
+  for (int64_t i = team0; i < a.n_list; i += nteams) {
+    const int64_t t = a.list[i];
+    const int64_t row = phase_row(a, t);
+    const int64_t beg = a.row_ptr[row];
+    const int m = (int)(a.row_ptr[row + 1] - beg);
+    const double s = a.slack[row];
+    const bool zero = !(s > 0.0);   // nothing is filled: P = 0, C = F = 0
+    bool known = zero;
+    bool flagged = false;   // the row searched last sweep
+    int g0 = 0, g1 = 0;
+    if (!zero && a.hint) {
+      const int h0 = a.hint[2 * t], h1 = a.hint[2 * t + 1];
+      if (h0 >= 0 && h1 >= 0) {
+        known = true;
+        flagged = ((h0 | h1) & HINT_SEARCHED) != 0;
+        const int c0 = h0 & HINT_COL, c1 = h1 & HINT_COL;
+        RankReg<WIDE> r;
+        if (c0 != HINT_COL) { r.load(a, c0); g0 = r.r0(); } else g0 = a.n;
+        if (c1 != HINT_COL) { r.load(a, c1); g1 = r.r1(); } else g1 = a.n;
+      }
+    }
+    // ---- pass A ----------------------------------------------------------
+    // one read of the row: lw (float, canonical per-lane order + fixed team
+    // tree), exact C(<g) and F(<g) per track, and {h, w} of the slots
+    // ranked in [g - W, g + W) per track.  The window buffer is
+    // double-buffered by row parity (cleared during the previous row's
+    // reduction).
+    const int par = (int)((i / nteams) & 1);
+    double2* win = s_win[slot][par];
+    const int wb0 = g0 - W, wb1 = g1 - W;
+    double fv[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    Fix xs[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // C0 F0 C1 F1
+    for_slots<TEAM, WIDE>(a, tid, row, beg, m,
+        [&](double l, double h, double2 w, const RankReg<WIDE>& rk) {
+          fv[0] = fma(l, w.x, fv[0]);
+          fv[1] = fma(l, w.y, fv[1]);
+          const int r0 = rk.r0(), r1 = rk.r1();
+          const bool b0 = r0 < g0, b1 = r1 < g1;
+          if (b0 | b1) {
+            const Fix hx = to_fix(h);
+            if (b0) { fix_add(xs[0], hx); fix_add(xs[1], to_fix(h * w.x)); }
+            if (b1) { fix_add(xs[2], hx); fix_add(xs[3], to_fix(h * w.y)); }
+          }
+          const unsigned d0 = (unsigned)(r0 - wb0), d1 = (unsigned)(r1 - wb1);
+          if (d0 < 2 * W) win[d0] = make_double2(h, w.x);
+          if (d1 < 2 * W) win[2 * W + d1] = make_double2(h, w.y);
+        });
+    team_sum_pass_a<TEAM>(fv, f_part, &s_win[slot][par ^ 1][0].x, 2 * SH::WIN);
+    team_sum_fix<TEAM, 4>(xs, x_part);
+    // ---- exact walk inside the window ------------------------------------
+    // need: 0 settled, 2 needs the bucketed search.  CTA teams walk the two
+    // tracks on warps 0 and 1 at once; a warp team walks both in turn.
+    {
+      const int lane = tid & 31, wid = tid >> 5;
+      auto walk = [&](auto oc) {
+        constexpr int o = decltype(oc)::value;
+        int p = o ? g1 : g0;
+        const bool settled = walk_track<W>(zero, known, s, a.n, lane,
+                                           win + o * 2 * W, xs[2 * o],
+                                           xs[2 * o + 1], p);
+        if (lane == 0) {
+          s_need[slot][o] = settled ? 0 : 2;
+          s_st[slot].P[o] = zero ? 0 : p;
+          s_x[slot][2 * o] = xs[2 * o];
+          s_x[slot][2 * o + 1] = xs[2 * o + 1];
+        }
+      };
+      using O0 = std::integral_constant<int, 0>;
+      using O1 = std::integral_constant<int, 1>;
+      if constexpr (TEAM == 32) {
+        walk(O0{});
+        walk(O1{});
+      } else if (wid == 0) {
+        walk(O0{});
+      } else if (wid == 1) {
+        walk(O1{});
+      }
+      if (tid == 0) {
+        s_lw[slot][0] = fv[0];
+        s_lw[slot][1] = fv[1];
+      }
+    }
+    team_sync();
+    int need[2] = {s_need[slot][0], s_need[slot][1]};
+    // ---- bucketed exact search for unsettled tracks ----------------------
+    if (need[0] | need[1]) {
+      SearchState& st = s_st[slot];
+      if (tid == 0) {
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          st.lo[o] = 0;
+          st.lg[o] = a.nbits;
+          st.cb[o] = 0;
+        }
+        st.act = (need[0] ? 1 : 0) | (need[1] ? 2 : 0);
+        if (a.miss_total) atomicAdd(a.miss_total + 1, 1ull);
+      }
+      team_sync();
+      search_levels<TEAM, WIDE>(a, tid, row, beg, m, s, st, hist, false);
+      // exact F(<P) of the searched tracks: one pass (integer sums)
+      const int q0 = need[0] ? st.P[0] : -1, q1 = need[1] ? st.P[1] : -1;
+      Fix fz[2] = {{0, 0}, {0, 0}};
+      for_slots<TEAM, WIDE, false>(a, tid, row, beg, m,
+          [&](double, double h, double2 w, const RankReg<WIDE>& rk) {
+            if (rk.r0() < q0) fix_add(fz[0], to_fix(h * w.x));
+            if (rk.r1() < q1) fix_add(fz[1], to_fix(h * w.y));
+          });
+      team_sum_fix<TEAM, 2>(fz, x_part);
+      if (tid == 0) {
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          if (need[o]) {
+            s_x[slot][2 * o + 1] = fz[o];
+            // C(<P) from the search, as the two-word form
+            const u128 c = st.C[o];
+            s_x[slot][2 * o] = Fix{(uint64_t)(c >> 44),
+                                   (uint64_t)(c & ((1ull << 44) - 1))};
+          }
+        }
+      }
+      team_sync();
+    }
+    if (tid == 0) {
+      const int p0 = s_st[slot].P[0], p1 = s_st[slot].P[1];
+      if (a.hint && (need[0] | need[1] | (int)flagged | (int)(p0 != g0) |
+                     (int)(p1 != g1))) {
+        // crossing columns for next sweep, flagged if this row searched
+        const int fl = (need[0] || need[1]) ? HINT_SEARCHED : 0;
+        a.hint[2 * t] = (p0 >= a.n ? HINT_COL : __ldg(a.perm0 + p0)) | fl;
+        a.hint[2 * t + 1] = (p1 >= a.n ? HINT_COL : __ldg(a.perm1 + p1)) | fl;
+      }
+      const Fix* x = s_x[slot];
+      a.out0[t] = row_value(s_lw[slot][0], fix_double(fixv(x[1])), s,
+                            fix_double(fixv(x[0])), p0, a.n, a.ws0);
+      a.out1[t] = row_value(s_lw[slot][1], fix_double(fixv(x[3])), s,
+                            fix_double(fixv(x[2])), p1, a.n, a.ws1);
+      if (a.miss_total && !(need[0] | need[1]) &&
+          (p0 != g0 || p1 != g1) && known && !zero)
+        atomicAdd(a.miss_total, 1ull);
+    }
+    team_sync();   // s_st / s_x / s_need are reused by the team's next row
   }
 }
 
@@ -1080,8 +1404,9 @@ struct Work {
   }
 };
 
-// Row classes of K5 by stored length (upper bounds, inclusive); a pure
-// function of the row, so the kernel a row gets never depends on its shard.
+// Row classes of K5 by stored length (upper bounds, inclusive; the last
+// class also takes every longer row); a pure function of the row, so the
+// kernel a row gets never depends on its shard.
 __constant__ int kClassHi[8] = {128, 256, 384, 512, 2048, 4096, 8192, 16384};
 
 __device__ __forceinline__ int row_class(int m) {
@@ -1128,7 +1453,9 @@ __global__ void k_class_scatter(const int64_t* row_ptr, const int64_t* fixed,
 
 void build_classes(const imp_imdp* h, Work& w, const int64_t* fixed_dev,
                    int64_t phase_rows, cudaStream_t s) {
-  if (h->max_row > 16384) fail(IMP_E_ARG, "row longer than 16384 stored entries");
+  // exact sums: per-row limb sums stay below 2^64 for < 2^20 slots (Fix)
+  if (h->max_row >= (1 << 20) - 2)
+    fail(IMP_E_ARG, "row longer than 2^20 - 3 stored entries");
   IMP_CUDA(cudaMemsetAsync(w.class_cnt.ptr, 0, w.class_cnt.bytes(), s));
   const int blocks = (int)std::max<int64_t>(
       1, std::min<int64_t>((phase_rows + 255) / 256, 148 * 8));
@@ -1170,7 +1497,9 @@ bool sweep_stats() {
 
 template <int TEAM, bool WIDE>
 void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
-  auto kern = k_sweep<TEAM, WIDE>;
+  void (*kern)(SweepArgs);
+  if constexpr (TEAM == 32) kern = k_sweep_warp<32, WIDE>;
+  else kern = k_sweep<TEAM, WIDE>;
   const int threads = TEAM == 32 ? 256 : TEAM;
   int per_sm = 0;
   IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,

@@ -270,3 +270,24 @@ def diagnose_convergence(imdp, spec="reach", mode="pessimistic",
     ph = run_phase(imdp, prog, lp, u_obj, eps, None, max_iterations,
                    mode=_lib.MODE_DIAGNOSE)
     return _report_k(ph.k0), _report_k(ph.k1)
+
+
+def row_values(t_min, t_max, r_min, r_max, a_min, a_max, weights, lp,
+               device=0):
+    """Greedy-LP values of dense rows (the reference's RowsSolver.values,
+    feasible.py:80-111) through K5: one value per row for the (n_s + 2)
+    weights [V, w_target, w_avoid].  Rows of any stored length (< 2^20)."""
+    from .abstraction import csr_from_dense, import_csr
+    t_min = np.asarray(t_min, dtype=float)
+    n_s = t_min.shape[1]
+    ptr, col, lo, hi = csr_from_dense(t_min, t_max)
+    h = import_csr(n_s, 1, 1, ptr, col, lo, hi, r_min, r_max, a_min, a_max,
+                   device=device)
+    w = _lib.as_f64(weights)
+    if len(w) != n_s + 2:
+        raise ValueError("weights must have n_s + 2 entries")
+    out = np.empty(t_min.shape[0])
+    _lib.check(_lib.load().imp_row_values(
+        h.raw, _lib.ptr(w, _lib.c_dbl), 1 if lp == "max" else 0,
+        _lib.ptr(out, _lib.c_dbl), 0))
+    return out
