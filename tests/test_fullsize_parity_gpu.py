@@ -1,0 +1,175 @@
+"""Full-size parity of the five BASELINE configs.
+
+Three layers, all at the configs' full sizes:
+
+1. Sweep-by-sweep against the oracle on every config.  The GPU runs phase 1
+   of the config's own synthesis for K = 1..5 iterations (run_phase with a
+   finite horizon: the same device loop, stopped early); for 48 sampled
+   states (boundary / interior / last) the oracle's LP + Bellman step
+   (oracle/iterate.py, pinned to the reference) maps the GPU's V after K-1
+   sweeps to V after K sweeps on the rows of those states (built as
+   one-state shards, bit-identical to the full build's rows).  Values within
+   1e-12, choices margin-aware.
+2. Against the reference run end to end at full size (fixtures made by
+   tests/golden/make_golden.py --only fullsize_*):
+   * dim14_verify: r / a vectors, per-row live counts and row sums, the
+     first 30 phase-1 V0 / V1 iterates, and the reference's own
+     ConvergenceError(k0, k1) at max_iterations = 30;
+   * robot2d_reachavoid: the same construction checksums, the first 6
+     V0 / V1 iterates and the phase-1 gap trace, iteration counts, p_min /
+     p_max and the policy (margin-aware, with the reference's top-2 margins).
+"""
+
+import numpy as np
+import pytest
+
+from paper_2401_03555_b200 import (ConvergenceError, build_abstraction,
+                                   synthesize_reach, verify)
+from paper_2401_03555_b200.config import benchmark
+from paper_2401_03555_b200.synthesis import run_phase
+
+from oracle import iterate as ORI
+
+from . import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = ("robot2d_reachavoid", "vehicle3d", "room5d", "bas7d_verify",
+           "dim14_verify")
+K_SWEEPS = 5
+N_STATES = 48
+
+
+def _phase1(cfg):
+    """(spec, lp, u_objective) of phase 1 of the config's synthesis
+    (synthesis.py:238-318, pessimistic)."""
+    if cfg.spec_type == "safety":
+        return "safety", "max", "min"
+    return "reach", "min", "max"
+
+
+def _sample_states(n_s, rng):
+    pick = rng.choice(n_s, size=min(N_STATES - 2, n_s), replace=False)
+    return np.unique(np.concatenate([[0, n_s - 1], pick]))
+
+
+def _state_model(cfg, labels, k, n_s):
+    """oracle Model of state k's rows (a one-state shard of the GPU build)."""
+    sh = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels,
+                           cfg.abstraction_options(), k_range=(int(k), 1))
+    ptr, col, lo, hi, r0, r1, a0, a1 = sh.csr()
+    rows = len(ptr) - 1
+    t_min = np.zeros((rows, n_s))
+    t_max = np.zeros((rows, n_s))
+    rr = np.repeat(np.arange(rows), np.diff(ptr))
+    t_min[rr, col] = lo
+    t_max[rr, col] = hi
+    return ORI.Model(1, sh.n_u, sh.n_w, t_min, t_max, r0, r1, a0, a1)
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_first_sweeps_match_oracle_at_full_size(name):
+    cfg = benchmark(name)
+    labels = cfg.labels()
+    im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels,
+                           cfg.abstraction_options())
+    n_s = im.n_s
+    spec, lp, u_obj = _phase1(cfg)
+    eps = cfg.eps
+    prev0, prev1 = np.zeros(n_s), np.ones(n_s)
+    trace = []
+    for k in range(1, K_SWEEPS + 1):
+        rep = run_phase(im, spec, lp, u_obj, eps, k, 10**6)
+        trace.append((rep.pair.v0.copy(), rep.pair.v1.copy(),
+                      rep.policy.copy()))
+    rng = np.random.default_rng(17)
+    states = _sample_states(n_s, rng)
+    models = {int(k): _state_model(cfg, labels, k, n_s) for k in states}
+    worst = 0.0
+    for k in range(K_SWEEPS):
+        v0, v1, pol = trace[k]
+        for s_idx, m in models.items():
+            want0, pick0 = ORI.bellman(m, prev0, lp, u_obj, spec)
+            want1, _ = ORI.bellman(m, prev1, lp, u_obj, spec)
+            worst = max(worst, abs(v0[s_idx] - want0[0]),
+                        abs(v1[s_idx] - want1[0]))
+            if m.n_u > 1 and pol[s_idx] != pick0[0]:
+                # margin-aware: the GPU's input is tie-optimal
+                rows = ORI.phase_rows(m, ORI.stacked(m))
+                tail = [1.0, 0.0] if spec == "reach" else [0.0, 1.0]
+                vals = rows.values(np.concatenate([prev0, tail]), lp)
+                per = vals.reshape(m.n_u, m.n_w)
+                per_u = per.min(axis=1) if u_obj == "max" else per.max(axis=1)
+                assert abs(per_u[pol[s_idx]] - per_u[pick0[0]]) <= 1e-12
+        prev0, prev1 = v0, v1
+    assert worst <= 1e-12, worst
+
+
+def _construction_checksums(g, im):
+    """Per-row live counts exact; r / a vectors within 1e-12; row sums and
+    column sums of t_max / t_min (a checksum over all entries) within 1e-9
+    (the entries agree; sums of up to 16 384 of them in different orders
+    differ by ~1e-13 relative)."""
+    ptr, col, lo, hi, r0, r1, a0, a1 = im.csr()
+    assert np.array_equal(np.diff(ptr), g["row_nnz"])
+    for key, got in (("r_min", r0), ("r_max", r1), ("a_min", a0),
+                     ("a_max", a1)):
+        assert np.max(np.abs(got - g[key])) <= 1e-12, key
+    rows = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    assert np.max(np.abs(np.bincount(rows, hi, len(ptr) - 1) -
+                         g["row_sum_max"])) <= 1e-9
+    assert np.max(np.abs(np.bincount(rows, lo, len(ptr) - 1) -
+                         g["row_sum_min"])) <= 1e-9
+    n_s = int(g["n_s"])
+    assert np.max(np.abs(np.bincount(col, hi, n_s) - g["t_max_colsum"])) \
+        <= 1e-9
+    assert np.max(np.abs(np.bincount(col, lo, n_s) - g["t_min_colsum"])) \
+        <= 1e-9
+
+
+def test_dim14_against_reference_run():
+    if not G.have("fullsize_dim14_verify"):
+        pytest.skip("fixture not generated")
+    g = G.load("fullsize_dim14_verify")
+    cfg = G.config_of(g)
+    im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
+                           cfg.abstraction_options())
+    _construction_checksums(g, im)
+    tr0, tr1 = g["trace_v0"], g["trace_v1"]
+    for k in (1, 2, 5, 10, len(tr0)):
+        rep = run_phase(im, "safety", "max", "min", cfg.eps, k, 10**6)
+        assert np.max(np.abs(rep.pair.v0 - tr0[k - 1])) <= 1e-12, k
+        assert np.max(np.abs(rep.pair.v1 - tr1[k - 1])) <= 1e-12, k
+    # the reference stops phase 1 at the iteration cap with the same k0/k1
+    assert str(g["error"]) == "ConvergenceError"
+    with pytest.raises(ConvergenceError) as exc:
+        verify(im, spec="safety", eps=cfg.eps, max_iterations=len(tr0))
+    want = (None if int(g["k0"]) < 0 else int(g["k0"]),
+            None if int(g["k1"]) < 0 else int(g["k1"]))
+    assert (exc.value.k0, exc.value.k1) == want
+
+
+def test_robot2d_reachavoid_against_reference_run():
+    if not G.have("fullsize_robot2d_reachavoid"):
+        pytest.skip("fixture not generated")
+    g = G.load("fullsize_robot2d_reachavoid")
+    cfg = G.config_of(g)
+    im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, cfg.labels(),
+                           cfg.abstraction_options())
+    _construction_checksums(g, im)
+    tr0, tr1 = g["trace_v0"], g["trace_v1"]
+    for k in range(1, len(tr0) + 1):
+        rep = run_phase(im, "reach", "min", "max", cfg.eps, k, 10**6)
+        assert np.max(np.abs(rep.pair.v0 - tr0[k - 1])) <= 1e-12, k
+        assert np.max(np.abs(rep.pair.v1 - tr1[k - 1])) <= 1e-12, k
+    c = synthesize_reach(im, mode=cfg.mode, eps=cfg.eps)
+    assert tuple(c.meta["iterations"]) == tuple(g["iterations"])
+    assert np.max(np.abs(c.p_min - g["p_min"])) <= 1e-9
+    assert np.max(np.abs(c.p_max - g["p_max"])) <= 1e-9
+    diff = c.policy != g["policy"]
+    tight = g["margin"] <= 1e-12
+    assert not np.any(diff & ~tight)
+    k = np.flatnonzero(diff)
+    per_u = g["per_u"]
+    assert np.all(np.abs(per_u[k, c.policy[k]] - per_u[k, g["policy"][k]])
+                  <= 1e-12)
