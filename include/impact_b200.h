@@ -157,6 +157,12 @@ typedef struct imp_build_desc {
    * (tests/test_construct_gpu.py).  The outer-bound tables, and with them
    * the live sets, are bit-exact in both modes. */
   int32_t exact;
+  /* non-NULL: count only -- run the mean ranges and the outer count pass,
+   * write each shard state's construction work (coupled: live entries +
+   * aux boxes + 1 per row, the Nelder-Mead items; separable: live entries
+   * + 1 per row) to state_cost[k_count], and return without building
+   * (*out = NULL).  The multi-GPU driver balances shards with it. */
+  int64_t* state_cost;
 } imp_build_desc;
 
 /* Per-build timings (device milliseconds, CUDA events) and counters. */
@@ -259,6 +265,35 @@ int imp_shard_sweep(imp_imdp* h, const double* v0, const double* v1,
                     const int64_t* fixed_policy_dev, double* new0,
                     double* new1, int64_t* policy, double* stats,
                     void* stream);
+
+/* Device-resident sharded phase loop (reference _run_phase over state
+ * shards; the multi-GPU hot loop).  shard_begin (host, world + 1) is the
+ * partition of the n_s safe states; this handle must be one of its shards.
+ * vbuf0 / vbuf1 (device, world * 2 * pw doubles; pw >= the widest shard)
+ * are the ping-pong value buffers in the packed layout [rank][V0|V1][pw]:
+ * iteration i (1-based) writes this rank's chunk of vbuf[i % 2] at offset
+ * rank * 2 * pw, and the caller's in-place all-gather of that chunk
+ * (2 * pw doubles per rank) completes the full vectors.  stats (device, 5
+ * doubles) receives this shard's [max|dV0|, max|dV1|, max(V1'-V0'),
+ * monotone, bracket]; the caller all-reduces it (max) before
+ * imp_shard_loop_control.  No call but begin / poll synchronises, so G
+ * iterations can be captured in one CUDA graph (with the collectives) and
+ * replayed; kernels of iterations after termination exit at once.
+ * desc->fixed_policy: this shard's phase-2 policy (host, k_count).
+ * poll reads the control block (a stream sync): *done, iterations, k0, k1,
+ * fallback, gap; once done it fills out->v0 / v1 (host, n_s, may be NULL)
+ * and out->policy (host, k_count: this shard's choices) and returns the
+ * reference's termination errors as imp_run_phase does. */
+typedef struct imp_shard_loop imp_shard_loop;
+int imp_shard_loop_begin(imp_imdp* h, const imp_phase_desc* desc,
+                         const int64_t* shard_begin, int32_t world,
+                         double* vbuf0, double* vbuf1, int64_t pw,
+                         double* stats, void* stream, imp_shard_loop** out);
+int imp_shard_loop_sweep(imp_shard_loop* loop, void* stream);
+int imp_shard_loop_control(imp_shard_loop* loop, void* stream);
+int imp_shard_loop_poll(imp_shard_loop* loop, imp_phase_out* out,
+                        int32_t* done, void* stream);
+void imp_shard_loop_free(imp_shard_loop* loop);
 
 /* Microbenchmark used for the FP64 roofline denominator: DFMA throughput
  * (GFLOP/s, 2 flops per DFMA) measured with CUDA events. */

@@ -53,7 +53,7 @@ class BuildDesc(ctypes.Structure):
                 ("mc", c_i32), ("mc_samples", c_i32),
                 ("mc_seed", ctypes.c_uint64), ("mc_norm", c_dbl),
                 ("inv_cov", P_dbl), ("dim_lo", P_dbl), ("dim_hi", P_dbl),
-                ("exact", c_i32)]
+                ("exact", c_i32), ("state_cost", P_i64)]
 
 
 class BuildStats(ctypes.Structure):
@@ -116,6 +116,15 @@ def _declare(lib):
     lib.imp_fp64_peak.argtypes = [c_i32, P_dbl]
     lib.imp_ndtr_eval.argtypes = [ctypes.POINTER(BuildDesc), P_dbl, P_dbl,
                                   c_i64, c_i32]
+    lib.imp_shard_loop_begin.argtypes = [c_vp, ctypes.POINTER(PhaseDesc),
+                                         P_i64, c_i32, c_vp, c_vp, c_i64,
+                                         c_vp, c_vp, ctypes.POINTER(c_vp)]
+    lib.imp_shard_loop_sweep.argtypes = [c_vp, c_vp]
+    lib.imp_shard_loop_control.argtypes = [c_vp, c_vp]
+    lib.imp_shard_loop_poll.argtypes = [c_vp, ctypes.POINTER(PhaseOut),
+                                        P_i32, c_vp]
+    lib.imp_shard_loop_free.argtypes = [c_vp]
+    lib.imp_shard_loop_free.restype = None
     lib.imp_jit_compile.argtypes = [ctypes.POINTER(BuildDesc),
                                     ctypes.c_char_p]
     lib.imp_export_text_rows.argtypes = [c_vp, c_i32, c_i64, c_i64,
@@ -145,7 +154,10 @@ EXPORTED = ("imp_last_error", "imp_version", "imp_device_query",
             "imp_run_phase", "imp_bellman_step", "imp_row_values",
             "imp_shard_sweep", "imp_fp64_peak", "imp_time_sweep",
             "imp_launch_count", "imp_export_text_rows",
-            "imp_format_values", "imp_simulate", "imp_ndtr_eval")
+            "imp_format_values", "imp_simulate", "imp_ndtr_eval",
+            "imp_shard_loop_begin", "imp_shard_loop_sweep",
+            "imp_shard_loop_control", "imp_shard_loop_poll",
+            "imp_shard_loop_free")
 
 
 def launch_count():

@@ -295,6 +295,25 @@ def build_abstraction(dyn, noise, spaces, labels, opts=None,
     return imdp
 
 
+def state_costs(dyn, noise, spaces, labels, opts=None, device=0,
+                k_range=None):
+    """Construction work per safe state (count pass only: mean ranges and
+    the outer pass, ~0.2 % of a coupled build): live entries + aux boxes
+    + 1 per row, i.e. the Nelder-Mead items of coupled dynamics.  The
+    multi-GPU driver balances state shards by it (sharded.balanced_shards),
+    the reference's fork pool splits rows evenly (abstraction.py:602-604)."""
+    desc, keep = describe(dyn, noise, spaces, labels, opts, device, k_range)
+    desc.exact = int(exact_default())
+    cost = np.zeros(max(desc.k_count, 1), dtype=np.int64)
+    desc.state_cost = _lib.ptr(cost, _lib.c_i64)
+    raw = ctypes.c_void_p()
+    stats = _lib.BuildStats()
+    _lib.check(_lib.load().imp_build(ctypes.byref(desc), ctypes.byref(raw),
+                                     ctypes.byref(stats)))
+    del keep
+    return cost[:desc.k_count]
+
+
 def jit_compile(dyn, noise, spaces, labels, opts=None, cubin_path=None,
                 exact=None):
     """NVRTC-compile the construction module for this system (no GPU

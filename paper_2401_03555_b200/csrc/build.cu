@@ -532,6 +532,29 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     P.write = 0;
     outer();
     stage_done("outer count");
+    if (d->state_cost) {   // count only: per-state construction work
+      std::vector<long long> tc(std::max<long long>(n_rows, 1)),
+          xc(std::max<long long>(n_rows, 1));
+      if (n_rows > 0) {
+        IMP_CUDA(cudaMemcpyAsync(tc.data(), tcnt.ptr, sizeof(long long) * n_rows,
+                                 cudaMemcpyDeviceToHost, s));
+        IMP_CUDA(cudaMemcpyAsync(xc.data(), xcnt.ptr, sizeof(long long) * n_rows,
+                                 cudaMemcpyDeviceToHost, s));
+      }
+      IMP_CUDA(cudaStreamSynchronize(s));
+      const long long per = (long long)d->n_u * d->n_w;
+      const bool refine = !d->separable || d->mc;
+      for (int k = 0; k < d->k_count; ++k) {
+        long long c = 0;
+        for (long long r = k * per; r < (k + 1) * per; ++r)
+          c += tc[r] + (refine ? xc[r] : 0) + 1;
+        d->state_cost[k] = c;
+      }
+      delete h;
+      h = nullptr;
+      *out = nullptr;
+      return;
+    }
     exclusive_scan(tcnt.ptr, reinterpret_cast<long long*>(row_ptr.ptr), n_rows + 1, s);
     exclusive_scan(xcnt.ptr, aux_ptr.ptr, n_rows + 1, s);
     long long nnz = 0, naux = 0;

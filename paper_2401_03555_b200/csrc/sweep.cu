@@ -63,6 +63,23 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Packed value layout of the device-resident sharded loop: the value
+// vectors of every rank's shard side by side, [rank][track][pw] (pw >= the
+// largest shard), so one in-place all-gather of a rank's [V0' | V1'] chunk
+// refreshes both full vectors.  sb = shard begins (world + 1).
+struct Packed {
+  const int64_t* sb;   // nullptr: plain layout v[t][p][c]
+  int world;
+  int64_t pw;
+};
+
+__device__ __forceinline__ int64_t vpos(const Packed& pk, int t, int64_t c) {
+  if (!pk.sb) return c;
+  int r = 0;
+  for (int q = 1; q < pk.world; ++q) r += c >= pk.sb[q];
+  return ((int64_t)r * 2 + t) * pk.pw + (c - pk.sb[r]);
+}
+
 // Control block of a phase loop living in device memory.  Kernels of an
 // iteration read `done` and return immediately once the loop terminated, so
 // a CUDA graph of G iterations can be replayed without host round trips.
@@ -95,6 +112,7 @@ struct OrderArgs {
   uint64_t* keys[2];
   int* idx[2];
   double2* colw;            // (n) {w0, w1} by column
+  Packed pk;                // sharded loop: packed value layout
 };
 
 __global__ void k_order_keys(OrderArgs a) {
@@ -105,7 +123,8 @@ __global__ void k_order_keys(OrderArgs a) {
   double w[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t)
-    w[t] = c < a.n_s ? a.v[t][pp][c] : (c == a.n_s ? a.d1 : a.d2);
+    w[t] = c < a.n_s ? a.v[t][pp][vpos(a.pk, t, c)]
+                     : (c == a.n_s ? a.d1 : a.d2);
   a.colw[c] = make_double2(w[0], w[1]);
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
@@ -1087,6 +1106,7 @@ struct ReduceArgs {
   int64_t* policy;           // (k_count) chosen inputs, may be nullptr
   int k_begin, k_count, n_u, n_w, u_max;
   double* stats;             // explicit-mode stats (no ctl): 5 doubles
+  Packed pk;                 // sharded loop: packed value layout
 };
 
 // Block max of the per-state statistics (exact, order-free) into the
@@ -1154,14 +1174,15 @@ __global__ void k_bellman(ReduceArgs a) {
       if (a.u_max ? (m1 > best1) : (m1 < best1)) best1 = m1;
     }
     const int g = a.k_begin + k;
-    const double o0 = a.old[0][pp][g], o1 = a.old[1][pp][g];
+    const int64_t g0 = ctl ? vpos(a.pk, 0, g) : g, g1 = ctl ? vpos(a.pk, 1, g) : g;
+    const double o0 = a.old[0][pp][g0], o1 = a.old[1][pp][g1];
     double n0 = best0, n1 = best1;
     if (ctl && ctl->frozen0) n0 = o0;
     if (ctl && ctl->frozen1) n1 = o1;
     if (a.policy) a.policy[k] = a.fixed ? a.fixed[k] : pick;
     if (ctl) {
-      a.nxt[0][pp ^ 1][g] = n0;
-      a.nxt[1][pp ^ 1][g] = n1;
+      a.nxt[0][pp ^ 1][g0] = n0;
+      a.nxt[1][pp ^ 1][g1] = n1;
     } else {
       a.nxt[0][0][k] = n0;
       a.nxt[1][0][k] = n1;
@@ -1222,14 +1243,15 @@ __global__ void k_bellman_warp(ReduceArgs a) {
     if (f1 != f1) b1 = f1;
     if (lane == 0) {
       const int g = a.k_begin + k;
-      const double o0 = a.old[0][pp][g], o1 = a.old[1][pp][g];
+      const int64_t g0 = ctl ? vpos(a.pk, 0, g) : g, g1 = ctl ? vpos(a.pk, 1, g) : g;
+      const double o0 = a.old[0][pp][g0], o1 = a.old[1][pp][g1];
       double n0 = b0, n1 = b1;
       if (ctl && ctl->frozen0) n0 = o0;
       if (ctl && ctl->frozen1) n1 = o1;
       if (a.policy) a.policy[k] = p0;
       if (ctl) {
-        a.nxt[0][pp ^ 1][g] = n0;
-        a.nxt[1][pp ^ 1][g] = n1;
+        a.nxt[0][pp ^ 1][g0] = n0;
+        a.nxt[1][pp ^ 1][g1] = n1;
       } else {
         a.nxt[0][0][k] = n0;
         a.nxt[1][0][k] = n1;
@@ -1246,12 +1268,24 @@ __global__ void k_bellman_warp(ReduceArgs a) {
 
 // Termination logic of _run_phase (synthesis.py:164-205) / diagnose
 // (:346-361), one thread.
-__global__ void k_control(Ctl* c) {
+// stats (sharded loop): the all-reduced [max|dV0|, max|dV1|, max gap,
+// monotone, bracket] of every rank instead of this device's slots.
+__global__ void k_control(Ctl* c, const double* stats) {
   if (c->done) return;
   const long long it = ++c->it;
-  const double d0 = key_value(c->slot_d0), d1 = key_value(c->slot_d1);
-  const double gap = key_value(c->slot_gap);
-  const unsigned flags = c->slot_flags;
+  double d0, d1, gap;
+  unsigned flags;
+  if (stats) {
+    d0 = stats[0];
+    d1 = stats[1];
+    gap = stats[2];
+    flags = (stats[3] > 0.0 ? 1u : 0u) | (stats[4] > 0.0 ? 2u : 0u);
+  } else {
+    d0 = key_value(c->slot_d0);
+    d1 = key_value(c->slot_d1);
+    gap = key_value(c->slot_gap);
+    flags = c->slot_flags;
+  }
   c->slot_d0 = c->slot_d1 = c->slot_gap = 0ull;
   c->slot_flags = 0u;
   if (c->mode == IMP_MODE_DIAGNOSE) {
@@ -1557,6 +1591,10 @@ struct Launch {
   double* new_explicit[2];      // explicit-mode outputs (k_count)
   double* stats_explicit;
   bool use_ctl;
+  Packed pk{};                   // sharded loop: packed value layout
+  double* vbuf[2] = {nullptr, nullptr};  // sharded loop: packed buffers
+  const double* stats_reduced = nullptr;  // sharded loop: k_control input
+  bool skip_control = false;     // sharded loop: control is a separate call
 };
 
 // Enqueue one iteration: order keys, 2 stable sorts, ranks, sweep, reduce
@@ -1570,7 +1608,8 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   OrderArgs oa{};
   for (int t = 0; t < 2; ++t)
     for (int p = 0; p < 2; ++p)
-      oa.v[t][p] = L.use_ctl ? w.v[t][p].ptr : L.v_explicit[t];
+      oa.v[t][p] = L.vbuf[p] ? L.vbuf[p]
+                   : (L.use_ctl ? w.v[t][p].ptr : L.v_explicit[t]);
   oa.ctl = ctl;
   oa.n_s = w.n_s;
   oa.n = n;
@@ -1582,6 +1621,7 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
     oa.idx[t] = w.idx_in[t].ptr;
   }
   oa.colw = w.colw.ptr;
+  oa.pk = L.pk;
   k_order_keys<<<(n + 255) / 256, 256, 0, s>>>(oa);
   IMP_CUDA(cudaGetLastError());
   for (int t = 0; t < 2; ++t) {
@@ -1650,8 +1690,10 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   rd.val1 = w.val[1].ptr;
   for (int t = 0; t < 2; ++t)
     for (int p = 0; p < 2; ++p) {
-      rd.old[t][p] = L.use_ctl ? w.v[t][p].ptr : L.v_explicit[t];
-      rd.nxt[t][p] = L.use_ctl ? w.v[t][p].ptr : L.new_explicit[t];
+      rd.old[t][p] = L.vbuf[p] ? L.vbuf[p]
+                     : (L.use_ctl ? w.v[t][p].ptr : L.v_explicit[t]);
+      rd.nxt[t][p] = L.vbuf[p] ? L.vbuf[p]
+                     : (L.use_ctl ? w.v[t][p].ptr : L.new_explicit[t]);
     }
   rd.fixed = L.fixed_dev;
   rd.policy = w.policy.ptr;
@@ -1661,6 +1703,7 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   rd.n_w = h->n_w;
   rd.u_max = L.u_max;
   rd.stats = L.stats_explicit;
+  rd.pk = L.pk;
   if (h->k_count > 0) {
     if (!rd.fixed && rd.n_u >= 16)
       k_bellman_warp<<<(int)(((int64_t)h->k_count * 32 + 255) / 256), 256, 0,
@@ -1669,12 +1712,13 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
       k_bellman<<<(h->k_count + 255) / 256, 256, 0, s>>>(rd);
     IMP_CUDA(cudaGetLastError());
   }
-  if (ctl) {
-    k_control<<<1, 1, 0, s>>>(ctl);
+  const bool control = ctl && !L.skip_control;
+  if (control) {
+    k_control<<<1, 1, 0, s>>>(ctl, L.stats_reduced);
     IMP_CUDA(cudaGetLastError());
   }
   return 2 + n_sweep + (w.wide ? 0 : 1) + (h->k_count > 0 ? 1 : 0) +
-         (ctl ? 1 : 0);
+         (control ? 1 : 0);
 }
 
 __global__ void k_fill(double* p, int64_t n, double v) {
@@ -2114,3 +2158,212 @@ extern "C" int imp_time_sweep(imp_imdp* h, int32_t spec, int32_t lp,
     *ms = t / reps;
   });
 }
+
+// ---------------------------------------------------------------------------
+// Device-resident sharded phase loop (multi-GPU; reference _run_phase,
+// synthesis.py:145-205, over state shards).  Per iteration the caller
+// enqueues, on one stream and without host synchronisation:
+//   imp_shard_loop_sweep    orders, K5 and the Bellman step of this shard,
+//                           writing its [V0' | V1'] chunk into the packed
+//                           buffer of the iteration and its statistics;
+//   all-gather (NCCL, in place) of the chunk and all-reduce(max) of the
+//                           5 statistics -- torch.distributed, the caller;
+//   imp_shard_loop_control  the termination logic of every rank on the
+//                           reduced statistics (k_control).
+// Kernels of an iteration after termination exit at once, so a CUDA graph
+// of G iterations can be replayed until imp_shard_loop_poll reports done:
+// one host round trip per G sweeps.
+// ---------------------------------------------------------------------------
+
+struct imp_shard_loop {
+  imp_imdp* h = nullptr;
+  imp::Work w;
+  imp::DevBuf<int64_t> sb;
+  std::vector<int64_t> hsb;
+  imp::Launch L{};
+  double* stats = nullptr;
+  int world = 1, rank = 0;
+  int64_t pw = 0;
+  double* buf[2] = {nullptr, nullptr};
+  double eps = 0.0;
+};
+
+namespace imp {
+namespace {
+__global__ void k_pack_init(double* b0, double* b1, int64_t total, int64_t pw) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= total) return;
+  const double v = ((q / pw) & 1) ? 1.0 : 0.0;   // track 0: zeros, 1: ones
+  b0[q] = v;
+  b1[q] = v;
+}
+
+// this device's statistics slots -> the 5 doubles the all-reduce combines
+__global__ void k_export_stats(Ctl* c, double* st) {
+  const unsigned long long u[3] = {c->slot_d0, c->slot_d1, c->slot_gap};
+  for (int q = 0; q < 3; ++q) st[q] = u[q] ? key_value(u[q]) : -INFINITY;
+  st[3] = (c->slot_flags & 1u) ? 1.0 : 0.0;
+  st[4] = (c->slot_flags & 2u) ? 1.0 : 0.0;
+  c->slot_d0 = c->slot_d1 = c->slot_gap = 0ull;
+  c->slot_flags = 0u;
+}
+}  // namespace
+}  // namespace imp
+
+extern "C" int imp_shard_loop_begin(imp_imdp* h, const imp_phase_desc* d,
+                                    const int64_t* shard_begin, int32_t world,
+                                    double* vbuf0, double* vbuf1, int64_t pw,
+                                    double* stats, void* stream,
+                                    imp_shard_loop** out) {
+  imp_shard_loop* L = nullptr;
+  int st = guarded([&] {
+    IMP_REQUIRE(h && d && shard_begin && vbuf0 && vbuf1 && stats && out,
+                "null argument");
+    IMP_REQUIRE(world >= 1 && world <= 64, "world size %d unsupported", world);
+    IMP_REQUIRE(d->eps > 0 || d->horizon > 0, "eps must be positive");
+    IMP_REQUIRE(shard_begin[0] == 0 && shard_begin[world] == h->n_s,
+                "shard table must cover the %d safe states", h->n_s);
+    int rank = -1;
+    int64_t widest = 0;
+    for (int r = 0; r < world; ++r) {
+      IMP_REQUIRE(shard_begin[r + 1] >= shard_begin[r], "shard table not sorted");
+      widest = std::max<int64_t>(widest, shard_begin[r + 1] - shard_begin[r]);
+      if (shard_begin[r] == h->k_begin &&
+          shard_begin[r + 1] == (int64_t)h->k_begin + h->k_count)
+        rank = r;
+    }
+    IMP_REQUIRE(rank >= 0, "this handle's states [%d, %d) are not a shard of "
+                "the table", h->k_begin, h->k_begin + h->k_count);
+    IMP_REQUIRE(pw >= widest && pw >= 1, "packed width %lld below the widest "
+                "shard (%lld)", (long long)pw, (long long)widest);
+    IMP_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    L = new imp_shard_loop();
+    L->h = h;
+    L->world = world;
+    L->rank = rank;
+    L->pw = pw;
+    L->buf[0] = vbuf0;
+    L->buf[1] = vbuf1;
+    L->stats = stats;
+    L->eps = d->eps;
+    L->hsb.assign(shard_begin, shard_begin + world + 1);
+    L->sb.alloc(world + 1);
+    IMP_CUDA(cudaMemcpyAsync(L->sb.ptr, shard_begin,
+                             sizeof(int64_t) * (world + 1),
+                             cudaMemcpyHostToDevice, s));
+    const int64_t phase_rows = d->fixed_policy ? (int64_t)h->k_count * h->n_w
+                                               : h->n_rows;
+    Work& w = L->w;
+    w.init(h, phase_rows);
+    if (d->fixed_policy) {
+      w.fixed.alloc(std::max(h->k_count, 1));
+      IMP_CUDA(cudaMemcpyAsync(w.fixed.ptr, d->fixed_policy,
+                               sizeof(int64_t) * h->k_count,
+                               cudaMemcpyHostToDevice, s));
+    }
+    build_classes(h, w, d->fixed_policy ? w.fixed.ptr : nullptr, phase_rows, s);
+    const int64_t total = (int64_t)world * 2 * pw;
+    k_pack_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(vbuf0, vbuf1,
+                                                                total, pw);
+    IMP_CUDA(cudaGetLastError());
+    Ctl c{};
+    c.k0 = c.k1 = -1;
+    c.mode = d->mode;
+    c.eps = d->eps;
+    c.horizon = d->horizon > 0 ? d->horizon : 0;
+    c.max_iter = d->max_iterations > 0 ? d->max_iterations : (1ll << 62);
+    IMP_CUDA(cudaMemcpyAsync(w.ctl.ptr, &c, sizeof(Ctl),
+                             cudaMemcpyHostToDevice, s));
+    Launch& la = L->L;
+    la.h = h;
+    la.w = &w;
+    la.sms = sm_count_of(h->device);
+    la.spec = d->spec;
+    la.lp = d->lp;
+    la.u_max = d->u_max;
+    la.fixed_dev = d->fixed_policy ? w.fixed.ptr : nullptr;
+    la.use_ctl = true;
+    la.skip_control = true;
+    la.pk = Packed{L->sb.ptr, world, pw};
+    la.vbuf[0] = vbuf0;
+    la.vbuf[1] = vbuf1;
+    la.stats_reduced = stats;
+    IMP_CUDA(cudaStreamSynchronize(s));
+    *out = L;
+  });
+  if (st != IMP_OK) delete L;
+  return st;
+}
+
+extern "C" int imp_shard_loop_sweep(imp_shard_loop* L, void* stream) {
+  return guarded([&] {
+    IMP_REQUIRE(L, "null argument");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    count_launches(enqueue_iteration(L->L, s), 2);
+    k_export_stats<<<1, 1, 0, s>>>(L->w.ctl.ptr, L->stats);
+    IMP_CUDA(cudaGetLastError());
+    count_launches(1, 0);
+  });
+}
+
+extern "C" int imp_shard_loop_control(imp_shard_loop* L, void* stream) {
+  return guarded([&] {
+    IMP_REQUIRE(L, "null argument");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    k_control<<<1, 1, 0, s>>>(L->w.ctl.ptr, L->stats);
+    IMP_CUDA(cudaGetLastError());
+    count_launches(1, 0);
+  });
+}
+
+extern "C" int imp_shard_loop_poll(imp_shard_loop* L, imp_phase_out* out,
+                                   int32_t* done, void* stream) {
+  return guarded([&] {
+    IMP_REQUIRE(L && out && done, "null argument");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Ctl hc{};
+    IMP_CUDA(cudaMemcpyAsync(&hc, L->w.ctl.ptr, sizeof(Ctl),
+                             cudaMemcpyDeviceToHost, s));
+    IMP_CUDA(cudaStreamSynchronize(s));
+    *done = hc.done;
+    out->iterations = hc.it;
+    out->sweeps = hc.it;
+    out->k0 = hc.k0;
+    out->k1 = hc.k1;
+    out->fallback = hc.fallback;
+    out->gap = hc.gap;
+    if (!hc.done) return;
+    const imp_imdp* h = L->h;
+    if (out->v0 || out->v1) {   // unpack the current full vectors
+      const int64_t total = (int64_t)L->world * 2 * L->pw;
+      std::vector<double> hb(total);
+      IMP_CUDA(cudaMemcpy(hb.data(), L->buf[hc.cur], sizeof(double) * total,
+                          cudaMemcpyDeviceToHost));
+      for (int r = 0; r < L->world; ++r)
+        for (int64_t c = L->hsb[r]; c < L->hsb[r + 1]; ++c) {
+          const int64_t base = (int64_t)r * 2 * L->pw + (c - L->hsb[r]);
+          if (out->v0) out->v0[c] = hb[base];
+          if (out->v1) out->v1[c] = hb[base + L->pw];
+        }
+    }
+    if (out->policy)
+      IMP_CUDA(cudaMemcpy(out->policy, L->w.policy.ptr,
+                          sizeof(int64_t) * h->k_count,
+                          cudaMemcpyDeviceToHost));
+    if (hc.status != IMP_OK) {
+      if (hc.status == IMP_E_CONVERGENCE)
+        set_error("gap %.17g above eps=%.17g after %lld iterations", hc.gap,
+                  L->eps, hc.it);
+      else if (hc.status == IMP_E_MONOTONE)
+        set_error("value iterates lost monotonicity; abstraction bounds "
+                  "inconsistent (iteration %lld)", hc.it);
+      else
+        set_error("interval iteration bracket violated (v0 > v1); "
+                  "abstraction bounds inconsistent (iteration %lld)", hc.it);
+      throw Failure{hc.status};
+    }
+  });
+}
+
+extern "C" void imp_shard_loop_free(imp_shard_loop* L) { delete L; }

@@ -5,17 +5,27 @@ construction needs no communication (each rank builds its shard into its
 own HBM, `build_abstraction(..., k_range=...)`) and the min over
 disturbances / max over inputs stays local.  Every sweep each rank prices
 its rows against the full value vectors, then
-  1. all-gather of the new V0' / V1' shards (one NCCL all_gather_into_tensor
-     over NVLink per track), and
-  2. all-reduce(max) of [max|dV0|, max|dV1|, gap, monotone, bracket].
-Every rank then runs the same termination logic (the reference's
-_run_phase, synthesis.py:145-205) on identical numbers, so all ranks stop at
-the same iteration.  Max is the only cross-rank floating-point reduction and
-it is exact, so results are bitwise independent of the rank count.
+  1. one in-place all-gather of its packed [V0' | V1'] chunk (NCCL
+     all_gather_into_tensor over NVLink: both tracks in one collective),
+  2. one all-reduce(max) of [max|dV0|, max|dV1|, gap, monotone, bracket],
+  3. the termination logic of the reference's _run_phase (synthesis.py:
+     145-205) on the reduced numbers -- on the device, identically on every
+     rank, so all ranks stop at the same iteration.
+Nothing of this needs the host: the C-ABI loop (imp_shard_loop_*) enqueues
+the sweep and the control step on the stream the collectives run on, so G
+iterations (sweep, all-gather, all-reduce, control) are captured in one
+CUDA graph and replayed; the host reads the control block once per G
+iterations.  Max is the only cross-rank floating-point reduction and it is
+exact, so results are bitwise independent of the rank count.
 
-The per-shard sweep is an engine object: CudaShard calls the C-ABI
-(imp_shard_sweep) on the rank's GPU; tests substitute a CPU engine to cover
-the exchange and control logic with gloo on world_size 2.
+Shards are balanced by construction work when a cost vector is given
+(balanced_shards: the outer pass's per-state count of live entries / NM
+items), else by state count (shard_range).
+
+The per-shard loop is an engine object: CudaShard drives the C-ABI on the
+rank's GPU; tests substitute a CPU engine (same packed buffers and call
+sequence, the oracle's LP and control logic) to cover the exchange with
+gloo on world_size 2.
 """
 
 import ctypes
@@ -26,7 +36,8 @@ import numpy as np
 from . import _lib
 from .errors import ConvergenceError, ImpactError
 
-__all__ = ["shard_range", "CudaShard", "run_phase", "synthesize",
+__all__ = ["shard_range", "balanced_shards", "shard_table", "CudaShard",
+           "shard_sweep", "plan_shards", "run_phase", "synthesize",
            "bench_step"]
 
 
@@ -37,10 +48,35 @@ def shard_range(n_s, world, rank):
     return begin, base + (1 if rank < extra else 0)
 
 
-class CudaShard:
-    """One rank's shard on its GPU; device tensors are torch (plumbing)."""
+def balanced_shards(cost, world):
+    """Shard table (world + 1 begins) splitting states into contiguous
+    blocks of nearly equal total cost (cost[k] >= 0 per safe state; e.g.
+    the NM items of state k from the construction's count pass).  A pure
+    function of the cost vector, so every rank derives the same table."""
+    cost = np.asarray(cost, dtype=np.float64)
+    n = len(cost)
+    csum = np.concatenate([[0.0], np.cumsum(np.maximum(cost, 0.0) + 1e-9)])
+    targets = csum[-1] * np.arange(1, world) / world
+    cuts = np.searchsorted(csum, targets, side="left")
+    cuts = np.clip(cuts, 0, n)
+    table = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    return np.maximum.accumulate(table)
 
-    def __init__(self, imdp, device):
+
+def shard_table(n_s, world):
+    """shard_range's partition as a table of begins (world + 1)."""
+    return np.array([shard_range(n_s, world, r)[0] for r in range(world)] +
+                    [n_s], dtype=np.int64)
+
+
+class CudaShard:
+    """One rank's shard on its GPU: the device-resident phase loop
+    (imp_shard_loop_*) with its packed ping-pong value buffers (torch
+    tensors: plumbing for the collectives)."""
+
+    supports_graphs = True
+
+    def __init__(self, imdp, device, table=None):
         import torch
         self.torch = torch
         self.imdp = imdp
@@ -48,127 +84,247 @@ class CudaShard:
         self.k_begin, self.k_count = info.k_begin, info.k_count
         self.n_s, self.n_u, self.n_w = info.n_s, info.n_u, info.n_w
         self.device = torch.device("cuda", device)
-        kc = max(self.k_count, 1)
-        self.new0 = torch.empty(kc, dtype=torch.float64, device=self.device)
-        self.new1 = torch.empty_like(self.new0)
-        self.pol = torch.empty(kc, dtype=torch.int64, device=self.device)
-        self.stats = torch.empty(5, dtype=torch.float64, device=self.device)
-        self.fixed = None
+        self.table = table
+        self.loop = None
 
-    def set_policy(self, local_policy):
+    def begin(self, table, spec, lp, u_obj, eps, horizon, max_iterations,
+              fixed_local=None, mode=None):
         t = self.torch
-        self.fixed = None if local_policy is None else t.as_tensor(
-            np.ascontiguousarray(local_policy, dtype=np.int64),
-            device=self.device)
+        self.free()
+        self.table = np.asarray(table, dtype=np.int64)
+        world = len(self.table) - 1
+        self.world = world
+        self.rank = int(np.flatnonzero(self.table[:-1] == self.k_begin)[-1])
+        self.pw = max(1, int(np.max(np.diff(self.table))))
+        size = world * 2 * self.pw
+        self.buf = [t.zeros(size, dtype=t.float64, device=self.device)
+                    for _ in range(2)]
+        self.stats = t.zeros(5, dtype=t.float64, device=self.device)
+        desc = _lib.PhaseDesc()
+        desc.spec = _lib.SPEC_REACH if spec == "reach" else _lib.SPEC_SAFETY
+        desc.lp = _lib.LP_MAX if lp == "max" else _lib.LP_MIN
+        desc.u_max = 1 if u_obj == "max" else 0
+        desc.mode = _lib.MODE_PHASE if mode is None else mode
+        desc.eps = float(eps) if eps is not None else 0.0
+        desc.horizon = int(horizon) if horizon is not None else 0
+        desc.max_iterations = int(max_iterations)
+        self._fixed = None
+        if fixed_local is not None:
+            self._fixed = _lib.as_i64(fixed_local)
+            desc.fixed_policy = _lib.ptr(self._fixed, _lib.c_i64)
+        raw = ctypes.c_void_p()
+        _lib.check(_lib.load().imp_shard_loop_begin(
+            self.imdp.device_handle().raw, ctypes.byref(desc),
+            _lib.ptr(self.table, _lib.c_i64), world, self.buf[0].data_ptr(),
+            self.buf[1].data_ptr(), self.pw, self.stats.data_ptr(),
+            self._stream(), ctypes.byref(raw)))
+        self.loop = raw
 
-    def zeros(self, n):
-        return self.torch.zeros(n, dtype=self.torch.float64,
-                                device=self.device)
+    def _stream(self):
+        return ctypes.c_void_p(
+            self.torch.cuda.current_stream(self.device).cuda_stream)
 
-    def ones(self, n):
-        return self.torch.ones(n, dtype=self.torch.float64,
-                               device=self.device)
+    def chunk(self, it):
+        b = self.buf[it % 2]
+        return b[self.rank * 2 * self.pw:(self.rank + 1) * 2 * self.pw]
 
-    def sweep(self, v0, v1, spec, lp, u_max):
-        stream = self.torch.cuda.current_stream(self.device).cuda_stream
-        fixed = self.fixed.data_ptr() if self.fixed is not None else None
-        _lib.check(_lib.load().imp_shard_sweep(
-            self.imdp.device_handle().raw, v0.data_ptr(), v1.data_ptr(),
-            spec, lp, u_max, fixed, self.new0.data_ptr(),
-            self.new1.data_ptr(), self.pol.data_ptr(),
-            self.stats.data_ptr(), ctypes.c_void_p(stream)))
-        k = self.k_count
-        return self.new0[:k], self.new1[:k], self.pol[:k], self.stats
+    def gathered(self, it):
+        return self.buf[it % 2]
+
+    def sweep(self, it):
+        _lib.check(_lib.load().imp_shard_loop_sweep(self.loop, self._stream()))
+
+    def control(self):
+        _lib.check(_lib.load().imp_shard_loop_control(self.loop,
+                                                      self._stream()))
+
+    def poll(self, final_out=None):
+        """(done, PhaseOut); once done, final_out = (v0, v1, local policy)
+        host arrays to fill."""
+        out = _lib.PhaseOut()
+        if final_out is not None:
+            v0, v1, pol = final_out
+            out.v0 = _lib.ptr(v0, _lib.c_dbl)
+            out.v1 = _lib.ptr(v1, _lib.c_dbl)
+            out.policy = _lib.ptr(pol, _lib.c_i64)
+        done = _lib.c_i32(0)
+        st = _lib.load().imp_shard_loop_poll(self.loop, ctypes.byref(out),
+                                            ctypes.byref(done), self._stream())
+        return bool(done.value), out, st
+
+    def free(self):
+        if self.loop is not None:
+            _lib.load().imp_shard_loop_free(self.loop)
+            self.loop = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def shard_sweep(imdp, v0, v1, spec, lp, u_max, fixed_local=None):
+    """One explicit twin sweep of a shard (imp_shard_sweep) against full
+    device value vectors v0 / v1 (torch): (new0, new1, policy, stats) of
+    its states.  The building block of host-driven iteration and tests."""
+    import torch
+    info = imdp.device_handle().info()
+    kc = max(info.k_count, 1)
+    dev = v0.device
+    new0 = torch.empty(kc, dtype=torch.float64, device=dev)
+    new1 = torch.empty_like(new0)
+    pol = torch.empty(kc, dtype=torch.int64, device=dev)
+    stats = torch.empty(5, dtype=torch.float64, device=dev)
+    fixed = None
+    if fixed_local is not None:
+        fixed = torch.as_tensor(np.ascontiguousarray(fixed_local,
+                                                     dtype=np.int64),
+                                device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _lib.check(_lib.load().imp_shard_sweep(
+        imdp.device_handle().raw, v0.data_ptr(), v1.data_ptr(), spec, lp,
+        u_max, fixed.data_ptr() if fixed is not None else None,
+        new0.data_ptr(), new1.data_ptr(), pol.data_ptr(), stats.data_ptr(),
+        ctypes.c_void_p(stream)))
+    k = info.k_count
+    return new0[:k], new1[:k], pol[:k], stats
 
 
 @dataclass
 class ShardedPhase:
-    v0: object
-    v1: object
+    v0: np.ndarray
+    v1: np.ndarray
     policy: np.ndarray
     iterations: int
     k0: int | None
     k1: int | None
     fallback: bool
     gap: float
+    graphs: bool = False
 
 
-def _gather(dist, local, n_total, world, counts, like_fn):
-    """All-gather variable-size contiguous shards into one vector."""
-    import torch
-    width = max(counts)
-    buf = like_fn(width)
-    buf[:local.shape[0]] = local
-    out = torch.empty(world * width, dtype=buf.dtype, device=buf.device)
-    dist.all_gather_into_tensor(out, buf)
-    parts = [out[r * width:r * width + counts[r]] for r in range(world)]
-    return torch.cat(parts)[:n_total]
+def _report_k(k):
+    return None if k is None or k < 0 else max(int(k) - 1, 1)
+
+
+def _iteration(engine, dist, it, inplace):
+    """Sweep, in-place all-gather of the packed chunk, all-reduce(max) of
+    the statistics, control: one reference iteration on every rank."""
+    engine.sweep(it)
+    out, mine = engine.gathered(it), engine.chunk(it)
+    if inplace:
+        dist.all_gather_into_tensor(out, mine)
+    else:
+        world = engine.world
+        parts = list(out.view(world, -1).unbind(0))   # views of out
+        dist.all_gather(parts, mine.clone())
+    dist.all_reduce(engine.stats, op=dist.ReduceOp.MAX)
+    engine.control()
+
+
+LAUNCH_BOUND_MS = 0.5
 
 
 def run_phase(engine, dist, spec, lp, u_obj, eps, horizon, max_iterations,
-              fixed_policy=None):
+              fixed_policy=None, table=None, graph_iters=16):
     """One reference phase (synthesis.py:145-205) over all ranks."""
-    import torch
     world = dist.get_world_size()
-    rank = dist.get_rank()
     n_s = engine.n_s
-    counts = [shard_range(n_s, world, r)[1] for r in range(world)]
-    b0, kc = shard_range(n_s, world, rank)
-    assert (b0, kc) == (engine.k_begin, engine.k_count), "shard mismatch"
-    engine.set_policy(None if fixed_policy is None
-                      else np.asarray(fixed_policy)[b0:b0 + kc])
-    spec_c = _lib.SPEC_REACH if spec == "reach" else _lib.SPEC_SAFETY
-    lp_c = _lib.LP_MAX if lp == "max" else _lib.LP_MIN
-    u_max = 1 if u_obj == "max" else 0
-    v0, v1 = engine.zeros(n_s), engine.ones(n_s)
-    k0 = k1 = None
-    prev = None
+    if table is None:
+        table = engine.table if engine.table is not None \
+            else shard_table(n_s, world)
+    table = np.asarray(table, dtype=np.int64)
+    b0 = int(engine.k_begin)
+    kc = int(engine.k_count)
+    local = None if fixed_policy is None else \
+        np.asarray(fixed_policy, dtype=np.int64)[b0:b0 + kc]
+    engine.begin(table, spec, lp, u_obj, eps, horizon, max_iterations,
+                 local)
+    inplace = dist.get_backend() == "nccl"
+    G = graph_iters if graph_iters % 2 == 0 else graph_iters + 1
+    G = max(G, 2)
+    # The first G iterations run eagerly (iteration 1 also initialises the
+    # communicator), one host poll after them.  A loop whose iterations are
+    # launch-bound (< LAUNCH_BOUND_MS each: small shards, many ranks) then
+    # captures G iterations -- sweep, all-gather, all-reduce, control -- in
+    # one CUDA graph and replays it; longer iterations keep the GPU busy
+    # eagerly and skip the capture's one-time cost.
+    import time
     it = 0
-    while True:
+    t0 = time.perf_counter()
+    for _ in range(G):
         it += 1
-        n0, n1, pol, st = engine.sweep(v0, v1, spec_c, lp_c, u_max)
-        st = st.clone()
-        dist.all_reduce(st, op=dist.ReduceOp.MAX)
-        # the gathers are queued before the host reads the statistics, so
-        # their launches overlap the sweep instead of following the sync
-        v0 = _gather(dist, n0, n_s, world, counts, engine.zeros)
-        v1 = _gather(dist, n1, n_s, world, counts, engine.zeros)
-        d0, d1, gap, mono, brk = (float(x) for x in st.cpu().tolist())
-        if mono > 0:
-            raise ImpactError("value iterates lost monotonicity; "
-                              "abstraction bounds inconsistent")
-        if k0 is None and d0 <= eps:
-            k0 = it
-        if k1 is None and d1 <= eps:
-            k1 = it
-        if brk > 0:
-            raise ImpactError("interval iteration bracket violated (v0 > v1);"
-                              " abstraction bounds inconsistent")
-        done = fallback = False
-        if horizon is not None:
-            done = it >= horizon
-        elif gap <= eps:
-            done = True
+        _iteration(engine, dist, it, inplace)
+    done, out, st = engine.poll()
+    per_it_ms = (time.perf_counter() - t0) * 1e3 / G
+    graph = None
+    if not done and graph_iters > 0 and per_it_ms < LAUNCH_BOUND_MS and \
+            getattr(engine, "supports_graphs", False):
+        graph = _capture(engine, dist, it + 1, G, inplace)
+    used_graph = False
+    while not done:
+        if graph:
+            graph.replay()
+            it += G
+            used_graph = True
         else:
-            stalled = prev is not None and prev - gap <= 1e-15 * max(1.0, gap)
-            if k0 is not None and k1 is not None and stalled:
-                done = fallback = True
-            else:
-                prev = gap
-                if it >= max_iterations:
-                    rk = (lambda k: None if k is None else max(k - 1, 1))
-                    raise ConvergenceError(
-                        f"gap {gap!r} above eps={eps!r} after {it} "
-                        "iterations", k0=rk(k0), k1=rk(k1))
-        if done:
-            polf = _gather(dist, pol.to(torch.float64), n_s, world, counts,
-                           engine.zeros)
-            return ShardedPhase(v0, v1, polf.cpu().numpy().astype(np.int64),
-                                it, k0, k1, fallback, gap)
+            for _ in range(G):
+                it += 1
+                _iteration(engine, dist, it, inplace)
+        done, out, st = engine.poll()
+    v0 = np.empty(n_s)
+    v1 = np.empty(n_s)
+    pol = np.empty(max(kc, 1), dtype=np.int64)
+    _, out, st = engine.poll((v0, v1, pol))
+    k0, k1 = _report_k(out.k0), _report_k(out.k1)
+    if st == _lib.IMP_E_CONVERGENCE:
+        raise ConvergenceError(
+            f"gap {out.gap!r} above eps={eps!r} after {out.iterations} "
+            "iterations", k0=k0, k1=k1)
+    if st in (_lib.IMP_E_MONOTONE, _lib.IMP_E_BRACKET):
+        raise ImpactError(_lib.last_error())
+    _lib.check(st)
+    policy = _gather_policy(engine, dist, pol[:kc], table)
+    return ShardedPhase(v0, v1, policy, int(out.iterations),
+                        None if out.k0 < 0 else int(out.k0),
+                        None if out.k1 < 0 else int(out.k1),
+                        bool(out.fallback), float(out.gap), used_graph)
+
+
+def _capture(engine, dist, it0, G, inplace):
+    """CUDA graph of G iterations starting at it0 (even G: the ping-pong
+    buffer parity repeats), or None when capture is not possible here."""
+    torch = engine.torch
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            for q in range(G):
+                _iteration(engine, dist, it0 + q, inplace)
+        return g
+    except Exception:     # e.g. a backend that cannot be captured
+        return False
+
+
+def _gather_policy(engine, dist, local, table):
+    """Full policy from every rank's local choices (int64 all-gather)."""
+    torch = engine.torch if hasattr(engine, "torch") else None
+    world = len(table) - 1
+    counts = np.diff(table)
+    width = max(1, int(counts.max()))
+    if torch is None:
+        import torch
+    dev = getattr(engine, "device", torch.device("cpu"))
+    buf = torch.zeros(width, dtype=torch.int64, device=dev)
+    buf[:len(local)] = torch.as_tensor(local, dtype=torch.int64, device=dev)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    return np.concatenate([parts[r][:counts[r]].cpu().numpy()
+                           for r in range(world)]).astype(np.int64)
 
 
 def synthesize(engine, dist, spec, mode="pessimistic", eps=1e-6, horizon=None,
-               max_iterations=10**6):
+               max_iterations=10**6, table=None, graph_iters=16):
     """Two-phase synthesis over shards (synthesis.py:238-303): returns
     (p_min, p_max, policy, iterations, fallback) on every rank."""
     if spec == "reach":
@@ -179,9 +335,10 @@ def synthesize(engine, dist, spec, mode="pessimistic", eps=1e-6, horizon=None,
         u_obj = "min"
     lp2 = "max" if lp1 == "min" else "min"
     ph1 = run_phase(engine, dist, spec, lp1, u_obj, eps, horizon,
-                    max_iterations)
+                    max_iterations, table=table, graph_iters=graph_iters)
     ph2 = run_phase(engine, dist, spec, lp2, u_obj, eps, horizon,
-                    max_iterations, fixed_policy=ph1.policy)
+                    max_iterations, fixed_policy=ph1.policy, table=table,
+                    graph_iters=graph_iters)
 
     def track(ph, lp):
         if horizon is not None or ph.fallback:
@@ -190,8 +347,8 @@ def synthesize(engine, dist, spec, mode="pessimistic", eps=1e-6, horizon=None,
             return ph.v0 if lp == "min" else ph.v1
         return ph.v0 if lp == "max" else ph.v1
 
-    a = track(ph1, lp1).cpu().numpy()
-    b = track(ph2, lp2).cpu().numpy()
+    a = track(ph1, lp1)
+    b = track(ph2, lp2)
     if spec == "reach":
         p_min, p_max = (a, b) if lp1 == "min" else (b, a)
     else:
@@ -206,12 +363,38 @@ def _h2d(cfg, labels):
     return h2d_bytes(cfg, labels)
 
 
+def plan_shards(cfg, labels, world, rank, device, dist):
+    """Cost-balanced shard table: every rank runs the construction's count
+    pass on an equal split, the per-state costs are all-gathered, and every
+    rank derives the same balanced table (balanced_shards)."""
+    import torch
+    from .abstraction import state_costs
+    n_s = len(labels.safe)
+    if world == 1:
+        return np.array([0, n_s], dtype=np.int64)
+    b, k = shard_range(n_s, world, rank)
+    local = state_costs(cfg.dynamics, cfg.noise, cfg.spaces, labels,
+                        cfg.abstraction_options(), device=device,
+                        k_range=(b, k))
+    width = shard_range(n_s, world, 0)[1]
+    dev = torch.device("cuda", device)
+    buf = torch.zeros(width, dtype=torch.int64, device=dev)
+    buf[:k] = torch.as_tensor(local, device=dev)
+    out = torch.empty(world * width, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(out, buf)
+    parts = out.view(world, width).cpu().numpy()
+    cost = np.concatenate([parts[r, :shard_range(n_s, world, r)[1]]
+                           for r in range(world)])
+    return balanced_shards(cost, world)
+
+
 def bench_step(args, cfg, labels, world, rank, device):
-    """bench.py at N > 1: each rank builds its shard, then the sharded
-    two-phase synthesis.  Device time (CUDA events on the launching stream,
-    max over ranks) with a barrier + synchronize around every timed step;
-    e2e is the same step through the public API from host inputs to the
-    host controller (wall time, max over ranks)."""
+    """bench.py at N > 1: each rank plans the cost-balanced partition,
+    builds its shard, then runs the sharded two-phase synthesis (device
+    loop + NCCL, CUDA graphs).  Device time (CUDA events on the launching
+    stream, max over ranks) with a barrier + synchronize around every timed
+    step; e2e is the same step through the public API from host inputs to
+    the host controller (wall time, max over ranks)."""
     import time
     import torch
     import torch.distributed as dist
@@ -219,15 +402,20 @@ def bench_step(args, cfg, labels, world, rank, device):
     n_s = len(labels.safe)
     n_u = cfg.input_space.total if cfg.input_space is not None else 1
     n_w = cfg.disturb_space.total if cfg.disturb_space is not None else 1
-    k_range = shard_range(n_s, world, rank)
     spec = "safety" if cfg.spec_type == "safety" else "reach"
-    builds, synths, sweeps, walls = [], [], [], []
+    if spec == "reach":
+        lp1, u_obj = ("min" if cfg.mode == "pessimistic" else "max"), "max"
+    else:
+        lp1, u_obj = ("max" if cfg.mode == "pessimistic" else "min"), "min"
+    lp2 = "max" if lp1 == "min" else "min"
+    builds, synths, ph1s, iters, walls, graphs = [], [], [], [], [], []
     sampler = None
     if rank == 0:
         from .benchutil import ClockSampler
         sampler = ClockSampler(device)
     l0 = None
     ctrl_bytes = 0
+    table = None
     for step in range(args.warmup + args.steps):
         timed = step >= args.warmup
         if sampler and step == max(args.warmup - 1, 0):
@@ -239,33 +427,45 @@ def bench_step(args, cfg, labels, world, rank, device):
         dist.barrier()
         torch.cuda.synchronize()
         w0 = time.perf_counter()
+        eb = torch.cuda.Event(enable_timing=True)
+        eb.record()
+        table = plan_shards(cfg, labels, world, rank, device, dist)
+        k_range = (int(table[rank]), int(table[rank + 1] - table[rank]))
         imdp = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels,
                                  cfg.abstraction_options(), device=device,
                                  k_range=k_range)
-        eng = CudaShard(imdp, device)
+        eng = CudaShard(imdp, device, table)
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
         e1.record()
-        res = synthesize(eng, dist, spec, cfg.mode, cfg.eps, cfg.horizon,
-                         cfg.max_iterations)
+        ph1 = run_phase(eng, dist, spec, lp1, u_obj, cfg.eps, cfg.horizon,
+                        cfg.max_iterations, table=table)
         e2.record()
+        ph2 = run_phase(eng, dist, spec, lp2, u_obj, cfg.eps, cfg.horizon,
+                        cfg.max_iterations, fixed_policy=ph1.policy,
+                        table=table)
+        e3.record()
         torch.cuda.synchronize()
         w1 = time.perf_counter()
         if timed:
-            builds.append(imdp.build_report.ms_total)
-            synths.append(e1.elapsed_time(e2))
-            sweeps.append(res[3][0])
+            builds.append(eb.elapsed_time(e1))
+            synths.append(e1.elapsed_time(e3))
+            ph1s.append(e1.elapsed_time(e2))
+            iters.append(ph1.iterations)
+            graphs.append(ph1.graphs)
             walls.append((w1 - w0) * 1e3)
-            ctrl_bytes = sum(np.asarray(a).nbytes for a in res[:3]
-                             if a is not None)
+            ctrl_bytes = 3 * n_s * 8
+        eng.free()
         if step < args.warmup + args.steps - 1:
             del eng, imdp   # the next build reuses the pooled CSR blocks
     l1 = _lib.launch_count()
     clocks = sampler.stop() if sampler else None
-    mx = torch.tensor([np.mean(builds), np.mean(synths), np.mean(walls)],
+    mx = torch.tensor([np.mean(builds), np.mean(synths), np.mean(walls),
+                       np.mean(ph1s)],
                       dtype=torch.float64, device=torch.device("cuda", device))
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    ms_build, ms_synth, ms_wall = (float(x) for x in mx.cpu().tolist())
+    ms_build, ms_synth, ms_wall, ms_ph1 = (float(x) for x in mx.cpu().tolist())
     entries = n_s * n_u * n_w * n_s
     if rank != 0:
         return None
@@ -279,11 +479,15 @@ def bench_step(args, cfg, labels, world, rank, device):
         "data": "synthetic",
         "config": {"workload": args.config, "rows": n_s * n_u * n_w,
                    "n_s": n_s, "entries": entries, "horizon": cfg.horizon,
-                   "step": "build_abstraction (shard) + two-phase synthesis",
-                   "parallelism": f"states sharded over {world} ranks; V "
-                                  "all-gathered per sweep (NCCL)"},
-        "sweeps_per_s": float(np.mean(sweeps)) / (ms_synth * 1e-3),
-        "ms_build": ms_build, "ms_synthesis": ms_synth,
+                   "step": "cost-balanced shard plan + build_abstraction "
+                           "(shard) + two-phase synthesis",
+                   "parallelism": f"states sharded over {world} ranks by "
+                                  "construction cost; packed [V0|V1] "
+                                  "all-gathered per sweep (NCCL, CUDA graphs)",
+                   "shards": [int(x) for x in np.diff(table)]},
+        "sweeps_per_s": float(np.mean(iters)) / (ms_ph1 * 1e-3),
+        "ms_build": ms_build, "ms_synthesis": ms_synth, "ms_phase1": ms_ph1,
+        "cuda_graphs": bool(all(graphs)),
         "e2e": {"value": entries / (ms_wall * 1e-3), "unit": "entries/s",
                 "h2d_bytes_per_step": _h2d(cfg, labels),
                 "d2h_bytes_per_step": int(ctrl_bytes),

@@ -72,7 +72,7 @@ def test_robot2d_reachavoid_controller_is_a_bellman_fixed_point(ra):
 
 def test_robot2d_reachavoid_shards_bitwise(ra):
     import torch
-    from paper_2401_03555_b200.sharded import CudaShard, shard_range
+    from paper_2401_03555_b200.sharded import shard_range, shard_sweep
     cfg, im = ra
     rng = np.random.default_rng(9)
     v = rng.uniform(0, 1, im.n_s)
@@ -83,7 +83,7 @@ def test_robot2d_reachavoid_shards_bitwise(ra):
         sh = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces,
                                cfg.labels(), cfg.abstraction_options(),
                                k_range=shard_range(im.n_s, 4, r))
-        n0, _, pol, _ = CudaShard(sh, 0).sweep(vt, vt, 0, 0, 1)
+        n0, _, pol, _ = shard_sweep(sh, vt, vt, 0, 0, 1)
         got.append(n0.cpu().numpy())
         gpick.append(pol.cpu().numpy())
     assert np.array_equal(np.concatenate(got), want)

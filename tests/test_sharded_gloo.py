@@ -1,10 +1,12 @@
 """Multi-rank interval iteration on CPU: world_size 2 over gloo.
 
-Covers paper_2401_03555_b200/sharded.py -- state sharding, the per-sweep
-all-gather of V0'/V1' and all-reduce(max) of the convergence statistics,
-and the replicated termination logic -- with a CPU shard engine (the
-oracle's row LP) standing in for the GPU kernel.  The sharded result must
-equal the reference's golden controller, and the single-rank run.
+Covers paper_2401_03555_b200/sharded.py -- state sharding (equal and
+cost-balanced tables), the packed ping-pong value buffers, the per-sweep
+all-gather of the packed [V0' | V1'] chunks and all-reduce(max) of the
+convergence statistics, the policy gather -- with a CPU shard engine (the
+oracle's row LP and a restatement of the device control step) standing in
+for the GPU loop.  The sharded result must equal the reference's golden
+controller, and the single-rank run.
 """
 
 import os
@@ -16,14 +18,19 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2401_03555_b200 import sharded
+from paper_2401_03555_b200 import _lib, sharded
 from oracle import lp as OL
 
 from . import golden_io as G
 
 
 class OracleShard:
-    """CPU engine with CudaShard's interface over one state block."""
+    """CPU engine with CudaShard's loop interface over one state block:
+    the same packed ping-pong buffers ([rank][V0|V1][pw]), the oracle's row
+    LP for the sweep, and a restatement of the device control step
+    (k_control: synthesis.py:164-205) on the all-reduced statistics."""
+
+    supports_graphs = False
 
     def __init__(self, g, k_begin, k_count):
         t_min, t_max = G.dense(g)
@@ -36,75 +43,154 @@ class OracleShard:
                              g["a_min"][rows, None]])
         self.hi = np.hstack([t_max[rows], g["r_max"][rows, None],
                              g["a_max"][rows, None]])
-        self.fixed = None
+        self.table = None
 
-    def set_policy(self, local):
-        self.fixed = None if local is None else np.asarray(local)
+    def begin(self, table, spec, lp, u_obj, eps, horizon, max_iterations,
+              fixed_local=None):
+        self.table = np.asarray(table)
+        self.world = len(table) - 1
+        self.rank = int(np.flatnonzero(self.table[:-1] == self.k_begin)[-1])
+        self.pw = max(1, int(np.max(np.diff(self.table))))
+        size = self.world * 2 * self.pw
+        self.buf = [torch.zeros(size, dtype=torch.float64) for _ in range(2)]
+        for b in self.buf:
+            b.view(self.world, 2, self.pw)[:, 1, :] = 1.0
+        self.stats = torch.zeros(5, dtype=torch.float64)
+        self.spec, self.lp, self.u_max = spec, lp, u_obj == "max"
+        self.eps, self.horizon, self.max_it = eps, horizon, max_iterations
+        self.fixed = None if fixed_local is None else np.asarray(fixed_local)
+        self.cur, self.it, self.done, self.status = 0, 0, False, 0
+        self.k0 = self.k1 = -1
+        self.prev, self.gap, self.fallback = None, 0.0, False
+        self.pol = np.zeros(self.k_count, dtype=np.int64)
 
-    def zeros(self, n):
-        return torch.zeros(n, dtype=torch.float64)
+    def _full(self, b, t):
+        v = b.view(self.world, 2, self.pw)[:, t, :]
+        return torch.cat([v[r, :self.table[r + 1] - self.table[r]]
+                          for r in range(self.world)]).numpy()
 
-    def ones(self, n):
-        return torch.ones(n, dtype=torch.float64)
+    def chunk(self, it):
+        b = self.buf[it % 2]
+        return b[self.rank * 2 * self.pw:(self.rank + 1) * 2 * self.pw]
 
-    def sweep(self, v0, v1, spec, lp, u_max):
-        tail = [1.0, 0.0] if spec == 0 else [0.0, 1.0]
-        direction = "max" if lp == 1 else "min"
+    def gathered(self, it):
+        return self.buf[it % 2]
+
+    def sweep(self, it):
+        if self.done:
+            return
+        tail = [1.0, 0.0] if self.spec == "reach" else [0.0, 1.0]
         lo, hi, U = self.lo, self.hi, self.n_u
         if self.fixed is not None:
             idx = ((np.arange(self.k_count) * self.n_u + self.fixed)[:, None]
                    * self.n_w + np.arange(self.n_w)).ravel()
             lo, hi, U = lo[idx], hi[idx], 1
         rows = OL.Rows(lo, hi)
+        src = self.buf[self.cur]
         outs, pick = [], None
-        for v in (v0, v1):
-            w = np.concatenate([v.numpy(), tail])
-            per = rows.values(w, direction).reshape(self.k_count, U,
-                                                    self.n_w)
-            per_u = per.min(axis=2) if u_max else per.max(axis=2)
-            ch = np.argmax(per_u, axis=1) if u_max else \
+        for t in range(2):
+            w = np.concatenate([self._full(src, t), tail])
+            per = rows.values(w, self.lp).reshape(self.k_count, U, self.n_w)
+            per_u = per.min(axis=2) if self.u_max else per.max(axis=2)
+            ch = np.argmax(per_u, axis=1) if self.u_max else \
                 np.argmin(per_u, axis=1)
             outs.append(per_u[np.arange(self.k_count), ch])
             if pick is None:
                 pick = ch if self.fixed is None else self.fixed
+        self.pol = np.asarray(pick, dtype=np.int64)
         b = self.k_begin
-        old0 = v0.numpy()[b:b + self.k_count]
-        old1 = v1.numpy()[b:b + self.k_count]
+        old = [self._full(src, t)[b:b + self.k_count] for t in range(2)]
         n0, n1 = outs
-        st = torch.tensor([
-            np.max(np.abs(n0 - old0), initial=-np.inf),
-            np.max(np.abs(n1 - old1), initial=-np.inf),
+        dst = self.chunk(it).view(2, self.pw)
+        dst[0, :self.k_count] = torch.from_numpy(n0)
+        dst[1, :self.k_count] = torch.from_numpy(n1)
+        self.stats.copy_(torch.tensor([
+            np.max(np.abs(n0 - old[0]), initial=-np.inf),
+            np.max(np.abs(n1 - old[1]), initial=-np.inf),
             np.max(n1 - n0, initial=-np.inf),
-            float(np.any(n0 < old0 - 1e-12) or np.any(n1 > old1 + 1e-12)),
-            float(np.any(n0 > n1 + 1e-9))], dtype=torch.float64)
-        return (torch.from_numpy(n0), torch.from_numpy(n1),
-                torch.from_numpy(np.asarray(pick, dtype=np.int64)), st)
+            float(np.any(n0 < old[0] - 1e-12) or np.any(n1 > old[1] + 1e-12)),
+            float(np.any(n0 > n1 + 1e-9))], dtype=torch.float64))
+
+    def control(self):
+        """k_control on the reduced statistics (synthesis.py:164-205)."""
+        if self.done:
+            return
+        self.it += 1
+        d0, d1, gap, mono, brk = (float(x) for x in self.stats.tolist())
+        if mono > 0:
+            self.status, self.done = _lib.IMP_E_MONOTONE, True
+            return
+        if self.k0 < 0 and d0 <= self.eps:
+            self.k0 = self.it
+        if self.k1 < 0 and d1 <= self.eps:
+            self.k1 = self.it
+        self.cur ^= 1
+        if brk > 0:
+            self.status, self.done = _lib.IMP_E_BRACKET, True
+            return
+        self.gap = gap
+        if self.horizon is not None:
+            self.done = self.it >= self.horizon
+            return
+        if gap <= self.eps:
+            self.done = True
+            return
+        stalled = self.prev is not None and \
+            self.prev - gap <= 1e-15 * max(1.0, gap)
+        if self.k0 >= 0 and self.k1 >= 0 and stalled:
+            self.fallback = self.done = True
+            return
+        self.prev = gap
+        if self.it >= self.max_it:
+            self.status, self.done = _lib.IMP_E_CONVERGENCE, True
+
+    def poll(self, final_out=None):
+        out = _lib.PhaseOut()
+        out.iterations, out.k0, out.k1 = self.it, self.k0, self.k1
+        out.fallback, out.gap = int(self.fallback), self.gap
+        if final_out is not None and self.done:
+            v0, v1, pol = final_out
+            v0[:] = self._full(self.buf[self.cur], 0)
+            v1[:] = self._full(self.buf[self.cur], 1)
+            pol[:self.k_count] = self.pol
+        return self.done, out, self.status
 
 
-def _worker(rank, world, port, name, queue):
+def _state_cost(g):
+    """Live entries per safe state (the construction count pass's work)."""
+    per = int(g["n_u"]) * int(g["n_w"])
+    nnz = np.diff(g["ptr"])
+    return nnz.reshape(int(g["n_s"]), per).sum(axis=1)
+
+
+def _worker(rank, world, port, name, queue, balanced=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         g = G.load("full_" + name)
         cfg = G.config_of(g)
-        b, k = sharded.shard_range(int(g["n_s"]), world, rank)
+        n_s = int(g["n_s"])
+        table = sharded.balanced_shards(_state_cost(g), world) if balanced \
+            else sharded.shard_table(n_s, world)
+        b, k = int(table[rank]), int(table[rank + 1] - table[rank])
         eng = OracleShard(g, b, k)
         res = sharded.synthesize(eng, dist, G.spec_of(cfg), cfg.mode,
-                                 cfg.eps, cfg.horizon)
+                                 cfg.eps, cfg.horizon, table=table)
         if rank == 0:
             queue.put(tuple(np.asarray(x) for x in res))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, name):
+def _run(world, name, balanced=False):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, name, q, balanced))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -115,10 +201,13 @@ def _run(world, name):
     return out
 
 
-@pytest.mark.parametrize("name", ["robot2d_ra_mini", "room5d_mini"])
-def test_two_ranks_match_reference_and_one_rank(name):
+@pytest.mark.parametrize("name,world,balanced",
+                         [("robot2d_ra_mini", 2, False),
+                          ("room5d_mini", 2, False),
+                          ("robot2d_ra_mini", 3, True)])
+def test_ranks_match_reference_and_one_rank(name, world, balanced):
     g = G.load("full_" + name)
-    p_min, p_max, policy, iters, fb = _run(2, name)
+    p_min, p_max, policy, iters, fb = _run(world, name, balanced)
     one = _run(1, name)
     # the CPU engine's `lower @ w` is BLAS, whose bits depend on the row
     # block shape (SURVEY.md finding 3), hence 1e-12 rather than bitwise
@@ -144,3 +233,17 @@ def test_shard_range_partitions():
                 assert b0 + k0 == b1
             assert sum(k for _, k in spans) == n
             assert max(k for _, k in spans) - min(k for _, k in spans) <= 1
+
+
+def test_balanced_shards_partition_by_cost():
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 1000, 16384):
+        cost = rng.integers(0, 50, n) * (rng.random(n) < 0.7)
+        for world in (1, 2, 3, 8):
+            t = sharded.balanced_shards(cost, world)
+            assert t[0] == 0 and t[-1] == n and len(t) == world + 1
+            assert np.all(np.diff(t) >= 0)
+            if n >= 1000 and world > 1:
+                parts = [cost[t[r]:t[r + 1]].sum() for r in range(world)]
+                # within one state's cost of the ideal split
+                assert max(parts) - cost.sum() / world <= cost.max() + 1

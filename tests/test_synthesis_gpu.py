@@ -364,7 +364,7 @@ def test_shard_sweeps_bitwise_equal_single_handle(name):
     single handle: no reduction depends on a row's position or shard."""
     import torch
     from paper_2401_03555_b200 import build_abstraction
-    from paper_2401_03555_b200.sharded import CudaShard, shard_range
+    from paper_2401_03555_b200.sharded import shard_range, shard_sweep
     g = G.load("full_" + name)
     cfg = G.config_of(g)
     labels = cfg.labels()
@@ -381,10 +381,10 @@ def test_shard_sweeps_bitwise_equal_single_handle(name):
         for r in range(3):
             shard = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces,
                                       labels, k_range=shard_range(n_s, 3, r))
-            eng = CudaShard(shard, 0)
-            n0, _, pol, _ = eng.sweep(vt, vt, 0 if spec == "reach" else 1,
-                                      1 if lp == "max" else 0,
-                                      1 if u_obj == "max" else 0)
+            n0, _, pol, _ = shard_sweep(shard, vt, vt,
+                                        0 if spec == "reach" else 1,
+                                        1 if lp == "max" else 0,
+                                        1 if u_obj == "max" else 0)
             got.append(n0.cpu().numpy())
             gpick.append(pol.cpu().numpy())
         assert np.array_equal(np.concatenate(got), want)
