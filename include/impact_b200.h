@@ -175,6 +175,7 @@ typedef struct imp_build_stats {
                                 nm_evals / nm_lane_slots = SIMT efficiency */
   int64_t nm_evals_shared;   /* of nm_evals: initial-simplex values a max
                                 run took from its min run (not evaluated) */
+  int64_t nnz_live;          /* stored entries with t_max > zero_cutoff   */
 } imp_build_stats;
 
 int imp_build(const imp_build_desc* desc, imp_imdp** out,
@@ -226,6 +227,11 @@ typedef struct imp_phase_out {
   double ms_sweep;       /* device time of the K5 launches alone, summed over
                           * the executed iterations (events captured into
                           * the loop's CUDA graph around each K5 group)      */
+  double* gap_log;       /* host (gap_log_cap) or NULL: max(v1 - v0) at every
+                          * 1000th iteration that continued -- the values the
+                          * reference logs (synthesis.py:204-205)           */
+  int64_t gap_log_cap;
+  int64_t gap_log_n;     /* entries written                                 */
 } imp_phase_out;
 
 /* Run one synthesis phase to termination (reference _run_phase,

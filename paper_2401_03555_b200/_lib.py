@@ -61,7 +61,8 @@ class BuildStats(ctypes.Structure):
                 ("ms_outer", c_dbl), ("ms_refine", c_dbl),
                 ("ms_assemble", c_dbl), ("nnz", c_i64),
                 ("nm_instances", c_i64), ("nm_evals", c_i64),
-                ("nm_lane_slots", c_i64), ("nm_evals_shared", c_i64)]
+                ("nm_lane_slots", c_i64), ("nm_evals_shared", c_i64),
+                ("nnz_live", c_i64)]
 
 
 class PhaseDesc(ctypes.Structure):
@@ -83,7 +84,9 @@ class PhaseOut(ctypes.Structure):
     _fields_ = [("v0", P_dbl), ("v1", P_dbl), ("policy", P_i64),
                 ("iterations", c_i64), ("k0", c_i64), ("k1", c_i64),
                 ("fallback", c_i32), ("gap", c_dbl), ("ms_device", c_dbl),
-                ("sweeps", c_i64), ("ms_sweep", c_dbl)]
+                ("sweeps", c_i64), ("ms_sweep", c_dbl),
+                ("gap_log", P_dbl), ("gap_log_cap", c_i64),
+                ("gap_log_n", c_i64)]
 
 
 _lib = None

@@ -14,6 +14,7 @@ tests do, is uploaded on first use.
 """
 
 import ctypes
+import logging
 import os
 import math
 from dataclasses import dataclass
@@ -25,6 +26,8 @@ from .errors import AbstractionError
 from .expr import lower_density, lower_dynamics
 from .grid import LabeledStates, Space, domain_box, multi_indices
 from .noise import CustomNoise, DiagonalNormal, FullNormal
+
+log = logging.getLogger(__name__)
 
 __all__ = ["AbstractionOptions", "RowIndex", "Imdp", "estimate_cost",
            "build_abstraction", "BuildReport"]
@@ -253,6 +256,7 @@ class BuildReport:
     rows: int
     entries: int          # rows * n_s: the reference's `d`
     nm_evals_shared: int = 0   # of nm_evals: initial-simplex values reused
+    nnz_live: int = 0          # stored entries with t_max > zero_cutoff
 
 
 def exact_default():
@@ -291,7 +295,12 @@ def build_abstraction(dyn, noise, spaces, labels, opts=None,
         stats.ms_total, stats.ms_mean_ranges, stats.ms_outer,
         stats.ms_refine, stats.ms_assemble, stats.nnz, stats.nm_instances,
         stats.nm_evals, stats.nm_lane_slots, rows, rows * desc.n_s,
-        stats.nm_evals_shared)
+        stats.nm_evals_shared, stats.nnz_live)
+    # the reference's build log line (abstraction.py:596-598)
+    entries = rows * desc.n_s
+    frac_zero = 1.0 - stats.nnz_live / entries if entries else 1.0
+    log.info("abstraction built: %d rows x %d cols, %.1f%% of t_max at zero",
+             rows, desc.n_s, 100 * frac_zero)
     return imdp
 
 

@@ -376,11 +376,12 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     DevBuf<unsigned long long> err(3);
     DevBuf<double> err_val(3);
     // [0] objective evals (the reference's count), [1] refine lane slots,
-    // [2] refine work counter, [3] evals saved by shared initial simplices
-    DevBuf<long long> evals(4);
+    // [2] refine work counter, [3] evals saved by shared initial simplices,
+    // [4] stored entries with t_max > zero_cutoff (k_assemble)
+    DevBuf<long long> evals(5);
     IMP_CUDA(cudaMemsetAsync(err.ptr, 0xff, 3 * sizeof(unsigned long long), s));
     IMP_CUDA(cudaMemsetAsync(err_val.ptr, 0, 3 * sizeof(double), s));
-    IMP_CUDA(cudaMemsetAsync(evals.ptr, 0, 4 * sizeof(long long), s));
+    IMP_CUDA(cudaMemsetAsync(evals.ptr, 0, 5 * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(tcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(xcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(raw.ptr, 0, (n_rows * 6 + 1) * sizeof(double), s));
@@ -622,13 +623,15 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
 
     unsigned long long herr[3];
     double hval[3];
-    long long hev = 0, hslots = 0, hshared = 0;
+    long long hev = 0, hslots = 0, hshared = 0, hlive = 0;
     IMP_CUDA(cudaMemcpy(herr, err.ptr, sizeof(herr), cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(hval, err_val.ptr, sizeof(hval), cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(&hev, evals.ptr, sizeof(hev), cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(&hslots, evals.ptr + 1, sizeof(hslots),
                         cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(&hshared, evals.ptr + 3, sizeof(hshared),
+                        cudaMemcpyDeviceToHost));
+    IMP_CUDA(cudaMemcpy(&hlive, evals.ptr + 4, sizeof(hlive),
                         cudaMemcpyDeviceToHost));
     const long long row0 = (long long)d->k_begin * d->n_u * d->n_w;
     if (herr[0] != ~0ull) {
@@ -662,6 +665,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
       stats->nm_evals = hev;
       stats->nm_lane_slots = hslots;
       stats->nm_evals_shared = hshared;
+      stats->nnz_live = hlive;
     }
     *out = h;
   });

@@ -1495,6 +1495,7 @@ extern "C" __global__ void k_assemble(BuildParams P) {
     }
     // clip t entries, t_min = min(t_min, t_max), low-cost zeroing
     double smin = 0.0, smax = 0.0;
+    unsigned live = 0;   // t_max > cutoff (the reference's sparsity log)
     for (long long q = b + lane; q < e; q += 32) {
       double hv = P.hi[q], lv = P.lo[q];
       if (IMP_MC) {     // abstraction.py:518-522
@@ -1509,9 +1510,13 @@ extern "C" __global__ void k_assemble(BuildParams P) {
       P.hi[q] = hi;
       smin += lo;
       smax += hi;
+      live += hi > P.cutoff;
     }
     smin = imp_warp_sum(smin);
     smax = imp_warp_sum(smax);
+    for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+    if (lane == 0 && live)
+      atomicAdd((unsigned long long*)P.evals + 4, (unsigned long long)live);
     rmin = imp_clip(rmin, 0.0, 1.0);
     rmax = imp_clip(rmax, 0.0, 1.0);
     rmin = fmin(rmin, rmax);

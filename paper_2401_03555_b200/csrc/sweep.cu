@@ -97,7 +97,12 @@ struct Ctl {
   long long horizon, max_iter;
   unsigned long long slot_d0, slot_d1, slot_gap;  // order_key-encoded maxima
   unsigned int slot_flags;                        // 1: monotone, 2: bracket
+  // the gap at every 1000th iteration that continued (the reference logs
+  // it, synthesis.py:204-205), first GAP_LOG of them
+  int gap_log_n;
+  double gap_log[256];
 };
+constexpr int GAP_LOG = 256;
 
 // ---------------------------------------------------------------------------
 // K4: global order of the (n_s + 2) weights of both tracks
@@ -1268,6 +1273,10 @@ __global__ void k_bellman_warp(ReduceArgs a) {
 
 // Termination logic of _run_phase (synthesis.py:164-205) / diagnose
 // (:346-361), one thread.
+__device__ __forceinline__ void log_gap(Ctl* c, long long it, double gap) {
+  if (it % 1000 == 0 && c->gap_log_n < GAP_LOG) c->gap_log[c->gap_log_n++] = gap;
+}
+
 // stats (sharded loop): the all-reduced [max|dV0|, max|dV1|, max gap,
 // monotone, bracket] of every rank instead of this device's slots.
 __global__ void k_control(Ctl* c, const double* stats) {
@@ -1304,6 +1313,7 @@ __global__ void k_control(Ctl* c, const double* stats) {
   c->gap = gap;
   if (c->horizon > 0) {
     if (it >= c->horizon) c->done = 1;
+    else log_gap(c, it, gap);
     return;
   }
   if (gap <= c->eps) { c->done = 1; return; }
@@ -1315,7 +1325,8 @@ __global__ void k_control(Ctl* c, const double* stats) {
   }
   c->prev_gap = gap;
   c->has_prev = 1;
-  if (it >= c->max_iter) { c->status = IMP_E_CONVERGENCE; c->done = 1; }
+  if (it >= c->max_iter) { c->status = IMP_E_CONVERGENCE; c->done = 1; return; }
+  log_gap(c, it, gap);
 }
 
 // ---------------------------------------------------------------------------
@@ -1874,6 +1885,11 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     out->k1 = hc.k1;
     out->fallback = hc.fallback;
     out->gap = hc.gap;
+    if (out->gap_log) {
+      const int nlog = std::min<int>(hc.gap_log_n, (int)out->gap_log_cap);
+      std::copy(hc.gap_log, hc.gap_log + nlog, out->gap_log);
+      out->gap_log_n = nlog;
+    }
     out->ms_device = ms;
     out->sweeps = hc.it;
     out->ms_sweep = ms_k5;
@@ -2333,6 +2349,11 @@ extern "C" int imp_shard_loop_poll(imp_shard_loop* L, imp_phase_out* out,
     out->k1 = hc.k1;
     out->fallback = hc.fallback;
     out->gap = hc.gap;
+    if (out->gap_log) {
+      const int nlog = std::min<int>(hc.gap_log_n, (int)out->gap_log_cap);
+      std::copy(hc.gap_log, hc.gap_log + nlog, out->gap_log);
+      out->gap_log_n = nlog;
+    }
     if (!hc.done) return;
     const imp_imdp* h = L->h;
     if (out->v0 || out->v1) {   // unpack the current full vectors

@@ -143,10 +143,13 @@ class CudaShard:
         host arrays to fill."""
         out = _lib.PhaseOut()
         if final_out is not None:
-            v0, v1, pol = final_out
+            v0, v1, pol = final_out[:3]
             out.v0 = _lib.ptr(v0, _lib.c_dbl)
             out.v1 = _lib.ptr(v1, _lib.c_dbl)
             out.policy = _lib.ptr(pol, _lib.c_i64)
+            if len(final_out) > 3:
+                out.gap_log = _lib.ptr(final_out[3], _lib.c_dbl)
+                out.gap_log_cap = len(final_out[3])
         done = _lib.c_i32(0)
         st = _lib.load().imp_shard_loop_poll(self.loop, ctypes.byref(out),
                                             ctypes.byref(done), self._stream())
@@ -276,8 +279,15 @@ def run_phase(engine, dist, spec, lp, u_obj, eps, horizon, max_iterations,
     v0 = np.empty(n_s)
     v1 = np.empty(n_s)
     pol = np.empty(max(kc, 1), dtype=np.int64)
-    _, out, st = engine.poll((v0, v1, pol))
+    gaps = np.empty(256)
+    _, out, st = engine.poll((v0, v1, pol, gaps))
     k0, k1 = _report_k(out.k0), _report_k(out.k1)
+    from .synthesis import log_phase
+    if dist.get_rank() == 0:
+        log_phase(gaps[:max(int(getattr(out, "gap_log_n", 0)), 0)],
+                  int(out.iterations), bool(out.fallback), float(out.gap),
+                  None if out.k0 < 0 else int(out.k0),
+                  None if out.k1 < 0 else int(out.k1))
     if st == _lib.IMP_E_CONVERGENCE:
         raise ConvergenceError(
             f"gap {out.gap!r} above eps={eps!r} after {out.iterations} "

@@ -11,6 +11,7 @@ replayed CUDA graphs; the host only picks value tracks and complements.
 """
 
 import ctypes
+import logging
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -21,6 +22,28 @@ from .errors import ConvergenceError, ImpactError
 __all__ = ["ValuePair", "Controller", "bellman_step", "synthesize_reach",
            "synthesize_safe", "verify", "diagnose_convergence",
            "PhaseReport"]
+
+log = logging.getLogger(__name__)
+
+GAP_LOG = 256   # gaps kept by the device loop: iterations 1000, 2000, ...
+
+
+def log_phase(gaps, iterations, fallback, gap, k0, k1):
+    """The reference's log lines for one phase (synthesis.py:190-194,
+    204-205), emitted after the device loop: the gap at every 1000th
+    iteration that continued, and the stalled-gap fallback warning."""
+    if log.isEnabledFor(logging.INFO):
+        for j, g in enumerate(gaps):
+            log.info("iteration %d: gap %.3e", 1000 * (j + 1), g)
+        if iterations // 1000 > len(gaps):
+            log.info("(gap log kept for the first %d thousand iterations)",
+                     len(gaps))
+    if fallback:
+        log.warning(
+            "gap stuck at %.3e with both bounds self-converged "
+            "(k0=%s, k1=%s); falling back to the value-iteration "
+            "result on the lower track", gap, _report_k(k0), _report_k(k1))
+
 
 DEFAULT_EPS = 1e-6
 DEFAULT_MAX_ITERATIONS = 10**6
@@ -114,14 +137,19 @@ def run_phase(imdp, spec, lp_direction, u_objective, eps, horizon,
     v0 = np.empty(n_s)
     v1 = np.empty(n_s)
     pol = np.empty(n_s, dtype=np.int64)
+    gaps = np.empty(GAP_LOG)
     out = _lib.PhaseOut()
     out.v0 = _lib.ptr(v0, _lib.c_dbl)
     out.v1 = _lib.ptr(v1, _lib.c_dbl)
     out.policy = _lib.ptr(pol, _lib.c_i64)
+    out.gap_log = _lib.ptr(gaps, _lib.c_dbl)
+    out.gap_log_cap = GAP_LOG
     st = _lib.load().imp_run_phase(h.raw, ctypes.byref(desc),
                                    ctypes.byref(out))
     k0 = None if out.k0 < 0 else int(out.k0)
     k1 = None if out.k1 < 0 else int(out.k1)
+    log_phase(gaps[:out.gap_log_n], out.iterations, bool(out.fallback),
+              float(out.gap), k0, k1)
     if st == _lib.IMP_E_CONVERGENCE:
         if mode == _lib.MODE_DIAGNOSE:
             raise ConvergenceError(

@@ -470,3 +470,37 @@ def test_diagnose_convergence_cap_reports_partial_horizons():
     with pytest.raises(ConvergenceError) as want:
         ORI.diagnose(om, spec=spec, eps=1e-6, max_iterations=60)
     assert (got.value.k0, got.value.k1) == (want.value.k0, want.value.k1)
+
+
+def test_reference_log_lines(caplog):
+    """The reference's log contract (abstraction.py:596-598, synthesis.py:
+    190-194, 204-205): the sparsity INFO line after a build, the gap INFO
+    line every 1000 iterations, and the stalled-gap fallback WARNING."""
+    import logging
+    from paper_2401_03555_b200 import build_abstraction
+    g = G.load("full_robot2d_ra_mini")
+    cfg = G.config_of(g)
+    with caplog.at_level(logging.INFO):
+        im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces,
+                               cfg.labels(), cfg.abstraction_options())
+    dense = G.dense(g)[1]
+    want = 100 * float(np.mean(dense <= 1e-12))
+    assert f"abstraction built: {im.n_rows} rows x {im.n_s} cols, " \
+           f"{want:.1f}% of t_max at zero" in caplog.text
+    caplog.clear()
+    # 2500 iterations of a slowly contracting chain: two gap lines
+    m = chain(0.0, 0.001, 0.999)
+    with caplog.at_level(logging.INFO):
+        synthesize_safe(m, eps=1e-300, horizon=2500)
+    assert "iteration 1000: gap" in caplog.text
+    assert "iteration 2000: gap" in caplog.text
+    assert "iteration 3000" not in caplog.text
+    caplog.clear()
+    # absorbing safe state: gap pinned at 1, both bounds self-converge ->
+    # fallback warning
+    ident = np.eye(2)
+    z = np.zeros(2)
+    with caplog.at_level(logging.WARNING):
+        c = synthesize_safe(make_imdp(ident, ident, z, z, z, z), eps=1e-6)
+    assert any(c.meta["fallback"])
+    assert "falling back to the value-iteration result" in caplog.text
