@@ -149,7 +149,7 @@ class OracleShard:
         out.iterations, out.k0, out.k1 = self.it, self.k0, self.k1
         out.fallback, out.gap = int(self.fallback), self.gap
         if final_out is not None and self.done:
-            v0, v1, pol = final_out
+            v0, v1, pol = final_out[:3]
             v0[:] = self._full(self.buf[self.cur], 0)
             v1[:] = self._full(self.buf[self.cur], 1)
             pol[:self.k_count] = self.pol
