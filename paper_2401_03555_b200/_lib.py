@@ -224,14 +224,6 @@ def ptr(a, ctype):
     return a.ctypes.data_as(ctypes.POINTER(ctype))
 
 
-def device_count():
-    """CUDA devices visible to the library's runtime (0 if none)."""
-    lib = load()
-    n = ctypes.c_int32(0)
-    st = lib.imp_device_query(0, ctypes.byref(n), None, None)
-    return 0 if st != IMP_OK else 1
-
-
 def fp64_peak_gflops(device=0):
     lib = load()
     out = c_dbl(0)

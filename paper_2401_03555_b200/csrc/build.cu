@@ -291,7 +291,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
                 "bad shard range");
     IMP_REQUIRE(d->dyn_source, "missing dynamics source");
     IMP_CUDA(cudaSetDevice(d->device));
-    int sms = 148;
+    int sms = 0;   // queried below
     IMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
                                     d->device));
     JitModule& M = jit(d->device, config_header(d), d->dyn_source);

@@ -257,7 +257,10 @@ extern "C" int imp_imdp_validate(const imp_imdp* h, double tol) {
     if (h->n_rows == 0) return;
     DevBuf<unsigned long long> bad(2);
     IMP_CUDA(cudaMemset(bad.ptr, 0xff, 2 * sizeof(unsigned long long)));
-    int blocks = (int)std::min<int64_t>((h->n_rows * 32 + 255) / 256, 148 * 64);
+    int sms = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    int blocks = (int)std::min<int64_t>((h->n_rows * 32 + 255) / 256,
+                                        (int64_t)std::max(sms, 1) * 64);
     k_validate<<<blocks, 256>>>(h->row_ptr.ptr, h->lo.ptr, h->hi.ptr,
                                 h->r_min.ptr, h->r_max.ptr, h->a_min.ptr,
                                 h->a_max.ptr, h->n_rows, tol, bad.ptr,
@@ -288,7 +291,7 @@ extern "C" int imp_fp64_peak(int device, double* gflops) {
   return guarded([&] {
     IMP_REQUIRE(gflops, "null argument");
     IMP_CUDA(cudaSetDevice(device));
-    int sms = 148;
+    int sms = 0;   // queried below
     IMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     DevBuf<double> o(1);
     const int iters = 4096, threads = 512, blocks = sms * 4;

@@ -38,6 +38,15 @@ namespace imp {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// SM count of a device (grid sizing: persistent grids are a multiple of it)
+inline int sm_count_of(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) !=
+          cudaSuccess || v <= 0)
+    v = 1;
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------
@@ -1362,7 +1371,8 @@ void finalize_imdp(imp_imdp* h, cudaStream_t s) {
   DevBuf<int> mr(1);
   IMP_CUDA(cudaMemsetAsync(mr.ptr, 0, sizeof(int), s));
   if (h->n_rows > 0) {
-    int blocks = (int)std::min<int64_t>((h->n_rows * 32 + 255) / 256, 148 * 64);
+    int blocks = (int)std::min<int64_t>((h->n_rows * 32 + 255) / 256,
+                                        (int64_t)sm_count_of(h->device) * 64);
     k_slack<<<blocks, 256, 0, s>>>(h->row_ptr.ptr, h->lo.ptr, h->hi.ptr,
                                    h->r_min.ptr, h->a_min.ptr, h->n_rows,
                                    h->slack.ptr, h->hd.ptr, mr.ptr);
@@ -1380,12 +1390,6 @@ void finalize_imdp(imp_imdp* h, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 
 namespace {
-
-int sm_count_of(int device) {
-  int v = 148;
-  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
-  return v;
-}
 
 // Per-handle working set of one phase / step.
 struct Work {
@@ -1503,7 +1507,8 @@ void build_classes(const imp_imdp* h, Work& w, const int64_t* fixed_dev,
     fail(IMP_E_ARG, "row longer than 2^20 - 3 stored entries");
   IMP_CUDA(cudaMemsetAsync(w.class_cnt.ptr, 0, w.class_cnt.bytes(), s));
   const int blocks = (int)std::max<int64_t>(
-      1, std::min<int64_t>((phase_rows + 255) / 256, 148 * 8));
+      1, std::min<int64_t>((phase_rows + 255) / 256,
+                           (int64_t)sm_count_of(h->device) * 8));
   if (phase_rows > 0) {
     k_class_count<<<blocks, 256, 0, s>>>(h->row_ptr.ptr, fixed_dev, h->n_u,
                                          h->n_w, phase_rows, w.class_cnt.ptr);

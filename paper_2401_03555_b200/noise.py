@@ -1,11 +1,11 @@
 """Noise models of the drop-in surface.
 
-Only diagonal Gaussian noise is on the B200 hot path (BASELINE.json
-north_star: "a product of erf differences for diagonal covariance").  The
-full-covariance and custom-density models (reference noise.py:41-95, the
-Monte Carlo path) are accepted as values so configs load, but
-build_abstraction rejects them: SURVEY.md section 8(f) lists them as a
-later row.
+Diagonal Gaussian noise is the B200 hot path (BASELINE.json north_star:
+"a product of erf differences for diagonal covariance").  The
+full-covariance and custom-density models (reference noise.py:41-95) take
+the Monte Carlo construction path: the same
+k_refine with the Monte Carlo objective, numpy's Philox streams restated
+on the device (csrc/rng.h).
 
 `interval_probability` here is the host restatement used for tests and
 host-side folding; the kernels use the cephes port in csrc/ndtr.h.
