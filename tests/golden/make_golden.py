@@ -546,6 +546,48 @@ def make_fullsize(name, workers, trace_iters=6, max_iter=None):
           flush=True)
 
 
+# --- the reference's optimistic mode and diagnose_convergence on minis ------
+
+def make_modes(name, workers):
+    """full_<name>'s abstraction (rebuilt by the reference), synthesized in
+    optimistic mode, and diagnose_convergence in both modes -- pins the
+    oracle's restatement of those paths (synthesis.py:238-361)."""
+    cfg = load(name)
+    labels = cfg.labels()
+    spaces = (cfg.state_space, cfg.input_space, cfg.disturb_space)
+    cfg.workers = workers
+    imdp = A.build_abstraction(cfg.dynamics, cfg.noise, spaces, labels,
+                               cfg.abstraction_options())
+    kind = cfg.spec_type
+    spec = "safety" if kind == "safety" else "reach"
+    out = dict(config=cfg_text(name))
+    kw = dict(mode="optimistic", eps=cfg.eps, horizon=cfg.horizon)
+    if imdp.input_space is None:
+        ctrl = S.verify(imdp, spec=spec, **kw)
+    elif kind == "safety":
+        ctrl = S.synthesize_safe(imdp, **kw)
+    else:
+        ctrl = S.synthesize_reach(imdp, **kw)
+    out.update(opt_p_min=ctrl.p_min, opt_p_max=ctrl.p_max,
+               opt_iterations=np.array(ctrl.meta["iterations"]),
+               opt_fallback=np.array(ctrl.meta["fallback"]),
+               opt_policy=(ctrl.policy if ctrl.policy is not None
+                           else np.zeros(0, np.int64)))
+    for mode in ("pessimistic", "optimistic"):
+        try:
+            k0, k1 = S.diagnose_convergence(imdp, spec=spec, mode=mode,
+                                            eps=cfg.eps, max_iterations=2000)
+            err = ""
+        except ConvergenceError as exc:
+            k0, k1, err = exc.k0, exc.k1, "ConvergenceError"
+        out[f"diag_{mode}"] = np.array([-1 if k0 is None else k0,
+                                        -1 if k1 is None else k1])
+        out[f"diag_{mode}_error"] = np.array(err)
+    np.savez_compressed(os.path.join(OUT, f"modes_{name}.npz"), **out)
+    print(f"modes_{name}: optimistic {out['opt_iterations']}, diagnose "
+          f"{out['diag_pessimistic']} / {out['diag_optimistic']}", flush=True)
+
+
 def make_ndtr():
     from scipy.special import ndtr
     rng = np.random.default_rng(2024)
@@ -594,6 +636,10 @@ def main():
         if on("full_" + name):
             make_full(name, args.workers,
                       max_iter=300 if name.startswith("dim") else None)
+    for name in ("robot2d_ra_mini", "room5d_mini", "dim6_mini",
+                 "bas4d_mini"):
+        if on("modes_" + name):
+            make_modes(name, args.workers)
     for name, n in SAMPLES.items():
         if on("rows_" + name):
             make_rows(name, n, args.workers)
