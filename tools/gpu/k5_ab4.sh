@@ -1,0 +1,5 @@
+python -m pytest tests/test_synthesis_gpu.py tests/test_fullsize_gpu.py tests/test_sharded_gpu.py -m gpu -q -x > gpurun_out/t14.log 2>&1
+for c in robot2d_reachavoid vehicle3d; do python tools/time_synth.py $c >> gpurun_out/ts14.txt 2>&1; done
+python tools/time_synth.py dim14_verify 100 >> gpurun_out/ts14.txt 2>&1
+python tools/time_synth.py room5d 100 >> gpurun_out/ts14.txt 2>&1
+python tools/prof_sweep.py vehicle3d >> gpurun_out/ts14.txt 2>&1
