@@ -1161,6 +1161,10 @@ __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
 #if IMP_NDTR_LEGACY
   (void)exp_tab;
   imp_ndtr_chunks<2 * IMP_N, IMP_NDTR_CHUNK>(arg, cdf, ndtr_tab);
+#elif IMP_NDTR_UNROLL   // measured slower (profiles/r02/k_refine_exact_knobs)
+#pragma unroll
+  for (int j = 0; j < 2 * IMP_N; j += IMP_NDTR_CHUNK)
+    imp_ndtr_batch_x<IMP_NDTR_CHUNK>(arg + j, cdf + j, ndtr_tab, exp_tab);
 #else
 #pragma unroll 1
   for (int j = 0; j < 2 * IMP_N; j += IMP_NDTR_CHUNK)
