@@ -11,7 +11,6 @@
 // Pipeline on one stream: stage 1 mean ranges -> stage 2 count -> CUB scan
 // -> stage 2 write -> [stage 3 NM refinement, coupled only] -> stage 4
 // assemble -> slack / row stats.  Device time per stage via CUDA events.
-#include <cub/device/device_scan.cuh>
 #include <nvrtc.h>
 
 #include <algorithm>
@@ -256,10 +255,8 @@ DevBuf<T> upload(const T* src, size_t n, cudaStream_t s) {
 
 void exclusive_scan(long long* counts, long long* out, int64_t n,
                     cudaStream_t s) {
-  size_t bytes = 0;
-  IMP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, out, n, s));
-  DevBuf<unsigned char> tmp(std::max<size_t>(bytes, 16));
-  IMP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, bytes, counts, out, n, s));
+  device_exclusive_scan(reinterpret_cast<const int64_t*>(counts),
+                        reinterpret_cast<int64_t*>(out), n, s);
 }
 
 struct Events {
@@ -651,7 +648,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     h->row_ptr = std::move(row_ptr);
     finalize_imdp(h, s);
     if (n_rows > 0)
-      count_launches(5 + (d->separable ? 0 : 1), 4);  // + slack kernel
+      count_launches(5 + (d->separable ? 0 : 1), 0);  // + slack kernel (scans count themselves)
     IMP_CUDA(cudaEventRecord(ev.e[5], s));
     IMP_CUDA(cudaEventSynchronize(ev.e[5]));
     if (stats) {

@@ -127,4 +127,10 @@ void finalize_imdp(imp_imdp* h, cudaStream_t s);  // slack + max_row
 // Kernel launches issued by this library (graph replays count every node):
 // our own kernels, and CUB primitive calls (sort / scan) separately.
 void count_launches(unsigned long long mine, unsigned long long cub);
+
+// out[i] = in[0] + ... + in[i-1] (exclusive scan of int64, out[0] = 0),
+// in-place allowed; our own block-scan kernels (no CUB): the CSR row
+// offsets of a build, the text offsets of an export.  Returns launches.
+int device_exclusive_scan(const int64_t* in, int64_t* out, int64_t n,
+                          cudaStream_t s);
 }

@@ -18,7 +18,6 @@
 //               length; a CUB scan over the block's rows gives line offsets
 //   k_row_text  one CTA per row: stored values at their offsets, zero runs
 //               by binary search of the entry whose extra prefix applies
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <vector>
@@ -142,13 +141,14 @@ __global__ void k_vec_text(const double* x, int64_t n, int64_t cols,
 // exclusive scan of len[0..n) in place into off[0..n]; returns the total
 int64_t scan_lengths(const int64_t* len, int64_t* off, int64_t n,
                      cudaStream_t s) {
-  IMP_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t), s));
-  if (n > 0) {
-    size_t bytes = 0;
-    IMP_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, len, off + 1, n, s));
-    DevBuf<unsigned char> tmp(std::max<size_t>(bytes, 16));
-    IMP_CUDA(cub::DeviceScan::InclusiveSum(tmp.ptr, bytes, len, off + 1, n, s));
-  }
+  // off[0..n] = exclusive scan of len[0..n) with off[n] the total: scan
+  // n + 1 values, the last one a zero appended behind a copy of len
+  DevBuf<int64_t> ext(n + 1);
+  if (n > 0)
+    IMP_CUDA(cudaMemcpyAsync(ext.ptr, len, sizeof(int64_t) * n,
+                             cudaMemcpyDeviceToDevice, s));
+  IMP_CUDA(cudaMemsetAsync(ext.ptr + n, 0, sizeof(int64_t), s));
+  device_exclusive_scan(ext.ptr, off, n + 1, s);
   int64_t total = 0;
   IMP_CUDA(cudaMemcpyAsync(&total, off + n, sizeof(int64_t),
                            cudaMemcpyDeviceToHost, s));
@@ -204,7 +204,7 @@ extern "C" int imp_export_text_rows(const imp_imdp* h, int32_t which,
     k_row_text<<<(unsigned)rows, XT, 0, s>>>(a);
     IMP_CUDA(cudaGetLastError());
     IMP_CUDA(cudaMemcpy(buf, text.ptr, total, cudaMemcpyDeviceToHost));
-    count_launches(2, 1);
+    count_launches(2, 0);
   });
 }
 
@@ -233,6 +233,6 @@ extern "C" int imp_format_values(const double* x, int64_t n, int64_t cols,
     k_vec_text<<<blocks, 256, 0, s>>>(dx.ptr, n, cols, off.ptr, text.ptr);
     IMP_CUDA(cudaGetLastError());
     IMP_CUDA(cudaMemcpy(buf, text.ptr, total, cudaMemcpyDeviceToHost));
-    count_launches(2, 1);
+    count_launches(2, 0);
   });
 }

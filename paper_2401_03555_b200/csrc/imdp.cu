@@ -14,6 +14,74 @@ namespace imp {
 static thread_local std::string g_last_error;
 static std::atomic<unsigned long long> g_mine{0}, g_cub{0};
 
+// --- exclusive scan of int64 (block tiles, then the tile sums) ------------
+namespace {
+constexpr int SCAN_THREADS = 1024, SCAN_PER = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER;
+
+__device__ __forceinline__ int64_t warp_incl_scan(int64_t v) {
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, v, d);
+    if ((threadIdx.x & 31) >= d) v += y;
+  }
+  return v;
+}
+
+// per tile: exclusive scan of the tile into out, the tile total into sums
+__global__ void __launch_bounds__(SCAN_THREADS)
+    k_scan_tiles(const int64_t* in, int64_t* out, int64_t* sums, int64_t n) {
+  __shared__ int64_t warp_tot[SCAN_THREADS / 32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE +
+                       (int64_t)threadIdx.x * SCAN_PER;
+  int64_t v[SCAN_PER], run = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0;
+    run += v[k];
+  }
+  const int64_t incl = warp_incl_scan(run);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t t = warp_incl_scan(warp_tot[lane]);
+    warp_tot[lane] = t;
+  }
+  __syncthreads();
+  int64_t off = incl - run + (warp > 0 ? warp_tot[warp - 1] : 0);
+#pragma unroll
+  for (int k = 0; k < SCAN_PER; ++k) {
+    const int64_t x = v[k];
+    if (base + k < n) out[base + k] = off;
+    off += x;
+  }
+  if (threadIdx.x == SCAN_THREADS - 1) sums[blockIdx.x] = off;
+}
+
+__global__ void k_scan_add(int64_t* out, const int64_t* offs, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += offs[i / SCAN_TILE];
+}
+}  // namespace
+
+int device_exclusive_scan(const int64_t* in, int64_t* out, int64_t n,
+                          cudaStream_t s) {
+  if (n <= 0) return 0;
+  const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  DevBuf<int64_t> sums(tiles);
+  k_scan_tiles<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, sums.ptr, n);
+  IMP_CUDA(cudaGetLastError());
+  int launches = 1;
+  if (tiles > 1) {
+    launches += device_exclusive_scan(sums.ptr, sums.ptr, tiles, s);
+    k_scan_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, sums.ptr, n);
+    IMP_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  count_launches(tiles > 1 ? 2 : 1, 0);   // this level's kernels
+  return launches;
+}
+
 void count_launches(unsigned long long mine, unsigned long long cub) {
   g_mine += mine;
   g_cub += cub;

@@ -24,7 +24,6 @@
 // shared order -- never on the hint, the path taken, its position or its
 // shard: bitwise-identical rows give bitwise-identical values.
 #include <type_traits>
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -180,6 +179,157 @@ __global__ void k_pack_ranks(const Ctl* ctl, int n, const int2* rank,
   if (ctl && ctl->done) return;
   int2 r = rank[c];
   rank16[c] = (unsigned)r.x | ((unsigned)r.y << 16);
+}
+
+// ---------------------------------------------------------------------------
+// K4 sort: the stable order of both tracks' keys (numpy's argsort(kind=
+// "stable"), feasible.py:53-58).  Sorting the pairs (key, column) by key
+// then column is a total order, so any correct sort is the stable sort.
+// Tiles of SORT_TILE pairs are bitonic-sorted in shared memory (one CTA per
+// tile and track), then merge passes of doubling width (merge path: each
+// thread finds its split of the two runs by binary search and merges a
+// fixed stretch of the output) until one run remains: 1 + ceil(log2(tiles))
+// launches for both tracks (robot2d: 1; vehicle3d: 3; bas7d: 7).
+// ---------------------------------------------------------------------------
+constexpr int SORT_TILE = 2048;      // pairs per tile (1 024 threads, 2 each)
+constexpr int MERGE_CHUNK = 2048;    // outputs per merge CTA
+constexpr int MERGE_THREADS = 256;   // -> 8 outputs per thread
+
+__device__ __forceinline__ bool pair_less(uint64_t ka, int ia, uint64_t kb,
+                                          int ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+struct SortArgs {
+  const Ctl* ctl;
+  int n;
+  uint64_t* key_in[2];   // per track
+  int* idx_in[2];
+  uint64_t* key_out[2];
+  int* idx_out[2];
+  int width;             // merge: current run width
+};
+
+__global__ void __launch_bounds__(SORT_TILE / 2)
+    k_sort_tiles(SortArgs a) {
+  if (a.ctl && a.ctl->done) return;
+  __shared__ uint64_t sk[SORT_TILE];
+  __shared__ int si[SORT_TILE];
+  const bool t1 = blockIdx.y != 0;   // track (selects, no local copies)
+  const uint64_t* kin = t1 ? a.key_in[1] : a.key_in[0];
+  const int* iin = t1 ? a.idx_in[1] : a.idx_in[0];
+  uint64_t* kout = t1 ? a.key_out[1] : a.key_out[0];
+  int* iout = t1 ? a.idx_out[1] : a.idx_out[0];
+  const int base = blockIdx.x * SORT_TILE;
+  for (int q = threadIdx.x; q < SORT_TILE; q += blockDim.x) {
+    const int g = base + q;
+    sk[q] = g < a.n ? kin[g] : ~0ull;
+    si[q] = g < a.n ? iin[g] : INT_MAX;
+  }
+  __syncthreads();
+  const int p = threadIdx.x;
+  for (int k = 2; k <= SORT_TILE; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int i = (p / j) * 2 * j + (p % j);
+      const int l = i + j;
+      const bool up = (i & k) == 0;
+      const uint64_t ki = sk[i], kl = sk[l];
+      const int ii = si[i], il = si[l];
+      if (pair_less(kl, il, ki, ii) == up) {
+        sk[i] = kl; si[i] = il;
+        sk[l] = ki; si[l] = ii;
+      }
+      __syncthreads();
+    }
+  }
+  for (int q = threadIdx.x; q < SORT_TILE; q += blockDim.x) {
+    const int g = base + q;
+    if (g < a.n) {
+      kout[g] = sk[q];
+      iout[g] = si[q];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(MERGE_THREADS) k_merge_pass(SortArgs a) {
+  if (a.ctl && a.ctl->done) return;
+  const bool t1 = blockIdx.y != 0;
+  const int w = a.width;
+  const int n = a.n;
+  constexpr int PER = MERGE_CHUNK / MERGE_THREADS;
+  const int o = blockIdx.x * MERGE_CHUNK + threadIdx.x * PER;  // output pos
+  if (o >= n) return;
+  const int pair0 = (o / (2 * w)) * 2 * w;
+  const int a0 = pair0, a1 = min(pair0 + w, n);
+  const int b0 = a1, b1 = min(pair0 + 2 * w, n);
+  const uint64_t* K = t1 ? a.key_in[1] : a.key_in[0];
+  const int* I = t1 ? a.idx_in[1] : a.idx_in[0];
+  const int na = a1 - a0, nb = b1 - b0;
+  const int diag = o - pair0;
+  // merge path: the number i of A elements among the first diag outputs
+  int lo = max(0, diag - nb), hi = min(diag, na);
+  while (lo < hi) {
+    const int i = (lo + hi) >> 1;
+    const int j = diag - 1 - i;
+    // A[i] comes before B[j] -> more A elements
+    if (pair_less(K[a0 + i], I[a0 + i], K[b0 + j], I[b0 + j])) lo = i + 1;
+    else hi = i;
+  }
+  int i = lo, j = diag - lo;
+  uint64_t* KO = t1 ? a.key_out[1] : a.key_out[0];
+  int* IO = t1 ? a.idx_out[1] : a.idx_out[0];
+  const int end = min(o + PER, pair0 + na + nb);
+  for (int q = o; q < end; ++q) {
+    bool take_a;
+    if (i >= na) take_a = false;
+    else if (j >= nb) take_a = true;
+    else take_a = pair_less(K[a0 + i], I[a0 + i], K[b0 + j], I[b0 + j]);
+    if (take_a) { KO[q] = K[a0 + i]; IO[q] = I[a0 + i]; ++i; }
+    else { KO[q] = K[b0 + j]; IO[q] = I[b0 + j]; ++j; }
+  }
+}
+
+// perm[t] (column by rank) of keys[t] / idx[t] (idx = column on entry;
+// keys and idx are clobbered).  Returns the number of launches.
+int launch_sort(const Ctl* ctl, int n, uint64_t* const keys[2],
+                int* const idx[2], uint64_t* const keys_tmp[2],
+                int* const perm[2], cudaStream_t s) {
+  if (n <= 0) return 0;
+  const int tiles = (n + SORT_TILE - 1) / SORT_TILE;
+  int passes = 0;
+  while ((SORT_TILE << passes) < n) ++passes;
+  // ping-pong so that the last pass writes (keys_tmp, perm)
+  SortArgs A{};
+  A.ctl = ctl;
+  A.n = n;
+  for (int t = 0; t < 2; ++t) {
+    A.key_in[t] = keys[t];
+    A.idx_in[t] = idx[t];
+    A.key_out[t] = passes % 2 ? keys[t] : keys_tmp[t];
+    A.idx_out[t] = passes % 2 ? idx[t] : perm[t];
+  }
+  k_sort_tiles<<<dim3(tiles, 2), SORT_TILE / 2, 0, s>>>(A);
+  IMP_CUDA(cudaGetLastError());
+  uint64_t* ck[2] = {A.key_out[0], A.key_out[1]};
+  int* ci[2] = {A.idx_out[0], A.idx_out[1]};
+  for (int p = 0; p < passes; ++p) {
+    SortArgs M{};
+    M.ctl = ctl;
+    M.n = n;
+    M.width = SORT_TILE << p;
+    for (int t = 0; t < 2; ++t) {
+      M.key_in[t] = ck[t];
+      M.idx_in[t] = ci[t];
+      M.key_out[t] = ck[t] == keys[t] ? keys_tmp[t] : keys[t];
+      M.idx_out[t] = ci[t] == idx[t] ? perm[t] : idx[t];
+      ck[t] = M.key_out[t];
+      ci[t] = M.idx_out[t];
+    }
+    k_merge_pass<<<dim3((n + MERGE_CHUNK - 1) / MERGE_CHUNK, 2),
+                   MERGE_THREADS, 0, s>>>(M);
+    IMP_CUDA(cudaGetLastError());
+  }
+  return 1 + passes;
 }
 
 // ---------------------------------------------------------------------------
@@ -1405,9 +1555,7 @@ struct Work {
   DevBuf<double> val[2];
   DevBuf<int> hint;                // warm-start crossing entries (2/row)
   DevBuf<int64_t> fixed, policy;
-  DevBuf<unsigned char> cub_tmp;
   DevBuf<Ctl> ctl;
-  size_t cub_bytes = 0;
   SweepArgs last_sweep{};   // arguments of the last enqueued K5 launch
   // K5 row classes: phase rows grouped by class (see launch_sweep)
   static constexpr int NCLASS = 8;
@@ -1443,12 +1591,7 @@ struct Work {
     rank.alloc(n);
     if (!wide) rank16.alloc(n);
     policy.alloc(std::max(h->k_count, 1));
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (uint64_t*)nullptr,
-                                    (uint64_t*)nullptr, (int*)nullptr,
-                                    (int*)nullptr, n);
-    cub_bytes = bytes;
-    cub_tmp.alloc(std::max<size_t>(bytes, 16));
+
     ctl.alloc(1);
   }
 };
@@ -1613,9 +1756,9 @@ struct Launch {
   bool skip_control = false;     // sharded loop: control is a separate call
 };
 
-// Enqueue one iteration: order keys, 2 stable sorts, ranks, sweep, reduce
-// (+ control when use_ctl).  Returns the number of our own kernels
-// enqueued (the two CUB sorts come on top).
+// Enqueue one iteration: order keys, the stable sorts of both tracks
+// (launch_sort), ranks, sweep, reduce (+ control when use_ctl).  Returns
+// the number of kernels enqueued (all of them ours).
 int enqueue_iteration(const Launch& L, cudaStream_t s) {
   const imp_imdp* h = L.h;
   Work& w = *L.w;
@@ -1640,12 +1783,11 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
   oa.pk = L.pk;
   k_order_keys<<<(n + 255) / 256, 256, 0, s>>>(oa);
   IMP_CUDA(cudaGetLastError());
-  for (int t = 0; t < 2; ++t) {
-    size_t bytes = w.cub_bytes;
-    IMP_CUDA(cub::DeviceRadixSort::SortPairs(
-        w.cub_tmp.ptr, bytes, w.keys_in[t].ptr, w.keys_out[t].ptr,
-        w.idx_in[t].ptr, w.perm[t].ptr, n, 0, 64, s));
-  }
+  uint64_t* const kin[2] = {w.keys_in[0].ptr, w.keys_in[1].ptr};
+  uint64_t* const kout[2] = {w.keys_out[0].ptr, w.keys_out[1].ptr};
+  int* const iin[2] = {w.idx_in[0].ptr, w.idx_in[1].ptr};
+  int* const pout[2] = {w.perm[0].ptr, w.perm[1].ptr};
+  const int n_sort = launch_sort(ctl, n, kin, iin, kout, pout, s);
   RankArgs ra{};
   ra.ctl = ctl;
   ra.n = n;
@@ -1733,7 +1875,7 @@ int enqueue_iteration(const Launch& L, cudaStream_t s) {
     k_control<<<1, 1, 0, s>>>(ctl, L.stats_reduced);
     IMP_CUDA(cudaGetLastError());
   }
-  return 2 + n_sweep + (w.wide ? 0 : 1) + (h->k_count > 0 ? 1 : 0) +
+  return 2 + n_sort + n_sweep + (w.wide ? 0 : 1) + (h->k_count > 0 ? 1 : 0) +
          (control ? 1 : 0);
 }
 
@@ -1841,7 +1983,7 @@ extern "C" int imp_run_phase(imp_imdp* h, const imp_phase_desc* d,
     long long it_before = 0;
     for (;;) {
       IMP_CUDA(cudaGraphLaunch(exec, s));
-      count_launches(per_graph, 2 * G);
+      count_launches(per_graph, 0);
       IMP_CUDA(cudaMemcpyAsync(&hc, w.ctl.ptr, sizeof(Ctl),
                                cudaMemcpyDeviceToHost, s));
       IMP_CUDA(cudaStreamSynchronize(s));
@@ -1975,7 +2117,7 @@ void explicit_step(imp_imdp* h, const double* v0, const double* v1, int spec,
   L.new_explicit[1] = new1;
   L.stats_explicit = stats;
   L.use_ctl = false;
-  count_launches(enqueue_iteration(L, s), 2);
+  count_launches(enqueue_iteration(L, s), 0);
   if (stats) {
     k_decode_stats<<<1, 1, 0, s>>>(stats);
     IMP_CUDA(cudaGetLastError());
@@ -2070,11 +2212,12 @@ extern "C" int imp_row_values(imp_imdp* h, const double* weights, int32_t lp,
     oa.colw = w.colw.ptr;
     k_order_keys<<<(n + 255) / 256, 256, 0, s>>>(oa);
     IMP_CUDA(cudaGetLastError());
-    for (int t = 0; t < 2; ++t) {
-      size_t bytes = w.cub_bytes;
-      IMP_CUDA(cub::DeviceRadixSort::SortPairs(
-          w.cub_tmp.ptr, bytes, w.keys_in[t].ptr, w.keys_out[t].ptr,
-          w.idx_in[t].ptr, w.perm[t].ptr, n, 0, 64, s));
+    {
+      uint64_t* const kin[2] = {w.keys_in[0].ptr, w.keys_in[1].ptr};
+      uint64_t* const kout[2] = {w.keys_out[0].ptr, w.keys_out[1].ptr};
+      int* const iin[2] = {w.idx_in[0].ptr, w.idx_in[1].ptr};
+      int* const pout[2] = {w.perm[0].ptr, w.perm[1].ptr};
+      launch_sort(nullptr, n, kin, iin, kout, pout, s);
     }
     RankArgs ra{};
     ra.n = n;
@@ -2321,7 +2464,7 @@ extern "C" int imp_shard_loop_sweep(imp_shard_loop* L, void* stream) {
   return guarded([&] {
     IMP_REQUIRE(L, "null argument");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    count_launches(enqueue_iteration(L->L, s), 2);
+    count_launches(enqueue_iteration(L->L, s), 0);
     k_export_stats<<<1, 1, 0, s>>>(L->w.ctl.ptr, L->stats);
     IMP_CUDA(cudaGetLastError());
     count_launches(1, 0);
