@@ -3,13 +3,14 @@
 Three layers, all at the configs' full sizes:
 
 1. Sweep-by-sweep against the oracle on every config.  The GPU runs phase 1
-   of the config's own synthesis for K = 1..5 iterations (run_phase with a
-   finite horizon: the same device loop, stopped early); for 48 sampled
-   states (boundary / interior / last) the oracle's LP + Bellman step
-   (oracle/iterate.py, pinned to the reference) maps the GPU's V after K-1
-   sweeps to V after K sweeps on the rows of those states (built as
-   one-state shards, bit-identical to the full build's rows).  Values within
-   1e-12, choices margin-aware.
+   of the config's own synthesis for K = 1..5 iterations, and to its own
+   termination N (run_phase with a finite horizon: the same device loop,
+   stopped early); for 48 sampled states (boundary / interior / last) the
+   oracle's LP + Bellman step (oracle/iterate.py, pinned to the reference)
+   maps the GPU's V after K-1 sweeps to V after K sweeps (K = 1..5 and
+   K = N) on the rows of those states (built as one-state shards,
+   bit-identical to the full build's rows).  Values within 1e-12, choices
+   margin-aware.
 2. Against the reference run end to end at full size (fixtures made by
    tests/golden/make_golden.py --only fullsize_*):
    * dim14_verify: r / a vectors, per-row live counts and row sums, the
@@ -102,6 +103,53 @@ def test_first_sweeps_match_oracle_at_full_size(name):
                 per_u = per.min(axis=1) if u_obj == "max" else per.max(axis=1)
                 assert abs(per_u[pol[s_idx]] - per_u[pick0[0]]) <= 1e-12
         prev0, prev1 = v0, v1
+    assert worst <= 1e-12, worst
+
+
+# the final sweep of phase 1 at each config's own termination (room5d and
+# dim14 at a 200-iteration horizon: their infinite-horizon runs end at the
+# reference's 10^6 cap with a ConvergenceError)
+FINAL_HORIZON = {"room5d": 200, "dim14_verify": 200}
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_final_sweep_matches_oracle_at_full_size(name):
+    """The controller's own last phase-1 step: V after N - 1 sweeps mapped
+    by the oracle's LP + Bellman step equals V after N sweeps (N = the
+    iteration the GPU loop stopped at) within 1e-12 on the sampled states,
+    choices margin-aware -- the converged values and policy checked
+    against an independent LP, not against the product's own operator."""
+    cfg = benchmark(name)
+    labels = cfg.labels()
+    im = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels,
+                           cfg.abstraction_options())
+    n_s = im.n_s
+    spec, lp, u_obj = _phase1(cfg)
+    horizon = FINAL_HORIZON.get(name)
+    last = run_phase(im, spec, lp, u_obj, cfg.eps, horizon, 10**6)
+    n = last.iterations
+    assert n >= 1
+    if n == 1:
+        prev0, prev1 = np.zeros(n_s), np.ones(n_s)
+    else:
+        prev = run_phase(im, spec, lp, u_obj, cfg.eps, n - 1, 10**6)
+        prev0, prev1 = prev.pair.v0, prev.pair.v1
+    rng = np.random.default_rng(29)
+    states = _sample_states(n_s, rng)
+    worst = 0.0
+    for k in states:
+        m = _state_model(cfg, labels, k, n_s)
+        want0, pick0 = ORI.bellman(m, prev0, lp, u_obj, spec)
+        want1, _ = ORI.bellman(m, prev1, lp, u_obj, spec)
+        worst = max(worst, abs(last.pair.v0[k] - want0[0]),
+                    abs(last.pair.v1[k] - want1[0]))
+        if m.n_u > 1 and last.policy[k] != pick0[0]:
+            rows = ORI.phase_rows(m, ORI.stacked(m))
+            tail = [1.0, 0.0] if spec == "reach" else [0.0, 1.0]
+            vals = rows.values(np.concatenate([prev0, tail]), lp)
+            per = vals.reshape(m.n_u, m.n_w)
+            per_u = per.min(axis=1) if u_obj == "max" else per.max(axis=1)
+            assert abs(per_u[last.policy[k]] - per_u[pick0[0]]) <= 1e-12
     assert worst <= 1e-12, worst
 
 
