@@ -145,9 +145,10 @@ std::string config_header(const imp_build_desc* d) {
     << (minb ? atoi(minb) : (d->n <= 4 ? 5 : d->n <= 8 ? 4 : 2))
     << "\n";
   const char* ch = getenv("IMPACT_NDTR_CHUNK");
-  // fast objective: two interleaved CDF chains per step (measured on the
-  // full vehicle3d build: 1.56e10 vs 1.53e10 evaluations/s for one)
-  o << "#define IMP_NDTR_CHUNK " << (ch ? atoi(ch) : 2)
+  // CDF chains interleaved per step: fast objective 2 (full vehicle3d
+  // build: 1.56e10 vs 1.53e10 evaluations/s for one), exact 1 (12.72 vs
+  // 12.87 s; profiles/r02/k_refine_exact_knobs_vehicle3d.txt)
+  o << "#define IMP_NDTR_CHUNK " << (ch ? atoi(ch) : exact_mode(d) ? 1 : 2)
     << "\n";
   const char* unr = getenv("IMPACT_NDTR_UNROLL");
   o << "#define IMP_NDTR_UNROLL " << (unr ? atoi(unr) : 0) << "\n";

@@ -310,7 +310,13 @@ struct NelderMead {
   // consume the value of the last point(); the iterate() it may owe is left
   // in `pend` so that a kernel can run it at one site for all its lanes
   __device__ void feed(double fp) {
-    bool iter = false, full = false;
+    // decisions per phase, then ONE block that moves an accepted point into
+    // the worst slot (a warp runs each divergent block once per trip, so the
+    // reflect-accept and second-candidate-take moves share it)
+    bool iter = false, full = false, replace = false;
+    int from = REF;
+    double newf = fp;
+    const int sw = slot(D);
     if (phase == NM_INIT || phase == NM_SHRINK) {
       fs(slot(v)) = fp;
       if (++v > D) {
@@ -320,8 +326,7 @@ struct NelderMead {
     } else if (phase == NM_REFLECT) {
       fr = fp;
       evals += 1;
-      const double f0 = fs(slot(0)), fsw = fs(slot(D - 1)), fw = fs(slot(D));
-      const int sw = slot(D);
+      const double f0 = fs(slot(0)), fsw = fs(slot(D - 1)), fw = fs(sw);
       if (fr < f0 || fr >= fsw) {
         kind = fr < f0 ? NM_EXPAND : (fr < fw ? NM_OUTSIDE : NM_INSIDE);
         const double coef = kind == NM_EXPAND ? 2.0 : 0.5;
@@ -334,27 +339,27 @@ struct NelderMead {
         }
         phase = NM_SECOND;
       } else {
-#pragma unroll
-        for (int d = 0; d < D; ++d) xs(sw, d) = xs(REF, d);
-        fs(sw) = fr;
-        iter = true;
+        replace = true;          // from REF, value fr
       }
     } else {  // NM_SECOND
       evals += 1;
-      const int sw = slot(D);
       const bool take = kind == NM_EXPAND ||
                         (kind == NM_OUTSIDE ? fp < fr : fp < fs(sw));
       if (take) {
         const bool use_c = kind != NM_EXPAND || fp < fr;
-        const int from = use_c ? CAND : REF;
-#pragma unroll
-        for (int d = 0; d < D; ++d) xs(sw, d) = xs(from, d);
-        fs(sw) = use_c ? fp : fr;
-        iter = true;
+        replace = true;
+        from = use_c ? CAND : REF;
+        newf = use_c ? fp : fr;
       } else {   // shrink: vertices 1..D move in point()
         v = 1;
         phase = NM_SHRINK;
       }
+    }
+    if (replace) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) xs(sw, d) = xs(from, d);
+      fs(sw) = newf;
+      iter = true;
     }
     if (iter) pend = full ? 2 : 1;
   }
