@@ -832,7 +832,7 @@ __device__ __forceinline__ double k5_margin(double c) {
 // ---------------------------------------------------------------------------
 template <int TEAM, bool WIDE>
 __global__ void __launch_bounds__(256, IMP_K5_TPSM / 256)
-    k_sweep_warp(SweepArgs a) {
+    k_sweep_warp(const __grid_constant__ SweepArgs a) {
   if (a.ctl && a.ctl->done) return;
   using SH = K5Shape<TEAM>;
   constexpr int TEAMS_PER_BLOCK = TEAM == 32 ? 8 : 1;
@@ -1105,12 +1105,18 @@ __device__ __forceinline__ bool walk_track(bool zero, bool known, double s,
   return false;
 }
 
+// CTA teams of <= IMP_K5_ENDSYNC threads end each row with a barrier
+// (room5d's 128-thread rows: 188 vs 183 phase-1 sweeps/s with it; the
+// 256 / 512 classes are faster without)
+#ifndef IMP_K5_ENDSYNC
+#define IMP_K5_ENDSYNC 128
+#endif
 template <int TEAM, bool WIDE>
 __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
                                   (TEAM == 32 ? 256 : TEAM) < IMP_K5_TPSM
                                       ? IMP_K5_TPSM / (TEAM == 32 ? 256 : TEAM)
                                       : 1)
-    k_sweep(SweepArgs a) {
+    k_sweep(const __grid_constant__ SweepArgs a) {
   if (a.ctl && a.ctl->done) return;
   using SH = K5Shape<TEAM>;
   constexpr int TEAMS_PER_BLOCK = TEAM == 32 ? 8 : 1;
@@ -1167,7 +1173,11 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     const int par = (int)((i / nteams) & 1);
     double2* win = s_win[slot][par];
     const int wb0 = g0 - W, wb1 = g1 - W;
-    double fv[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    // clear the next row's window buffer: its last readers (the previous
+    // row's walk) finished before the previous row's second barrier
+    for (int q = tid; q < 2 * SH::WIN; q += TEAM)
+      (&s_win[slot][par ^ 1][0].x)[q] = 0.0;
+    double fv[2] = {0.0, 0.0};
     Fix xs[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // C0 F0 C1 F1
     for_slots<TEAM, WIDE>(a, tid, row, beg, m,
         [&](double l, double h, double2 w, const RankReg<WIDE>& rk) {
@@ -1184,42 +1194,56 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
           if (d0 < 2 * W) win[d0] = make_double2(h, w.x);
           if (d1 < 2 * W) win[2 * W + d1] = make_double2(h, w.y);
         });
-    team_sum_pass_a<TEAM>(fv, f_part, &s_win[slot][par ^ 1][0].x, 2 * SH::WIN);
-    team_sum_fix<TEAM, 4>(xs, x_part);
-    // ---- exact walk inside the window ------------------------------------
-    // need: 0 settled, 2 needs the bucketed search.  CTA teams walk the two
-    // tracks on warps 0 and 1 at once; a warp team walks both in turn.
+    // ---- team sums + exact walk inside the window -------------------------
+    // Warp partials of lw (float) and C, F (exact) go to shared memory
+    // behind ONE barrier; warp o then finishes track o's sums itself (the
+    // float lw with the fixed tree of team_sum_f: lane w adds warp w's
+    // partial, then a butterfly) and walks its window.  need: 0 settled,
+    // 2 needs the bucketed search.
+    static_assert(TEAM > 32, "k_sweep: CTA teams");
     {
+      constexpr int NW = SH::NW;
       const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) fv[k] = warp_sum(fv[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xs[k] = warp_sum_fix(xs[k]);
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) f_part[k * NW + wid] = fv[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x_part[k * NW + wid] = xs[k];
+      }
+      __syncthreads();
       auto walk = [&](auto oc) {
         constexpr int o = decltype(oc)::value;
+        Fix C = warp_sum_fix(lane < NW ? x_part[(2 * o) * NW + lane]
+                                       : Fix{0, 0});
+        Fix F = warp_sum_fix(lane < NW ? x_part[(2 * o + 1) * NW + lane]
+                                       : Fix{0, 0});
         int p = o ? g1 : g0;
         const bool settled = walk_track<W>(zero, known, s, a.n, lane,
-                                           win + o * 2 * W, xs[2 * o],
-                                           xs[2 * o + 1], p);
+                                           win + o * 2 * W, C, F, p);
         if (lane == 0) {
           s_need[slot][o] = settled ? 0 : 2;
           s_st[slot].P[o] = zero ? 0 : p;
-          s_x[slot][2 * o] = xs[2 * o];
-          s_x[slot][2 * o + 1] = xs[2 * o + 1];
+          s_x[slot][2 * o] = C;
+          s_x[slot][2 * o + 1] = F;
         }
       };
-      using O0 = std::integral_constant<int, 0>;
-      using O1 = std::integral_constant<int, 1>;
-      if constexpr (TEAM == 32) {
-        walk(O0{});
-        walk(O1{});
-      } else if (wid == 0) {
-        walk(O0{});
+      if (wid == 0) {
+        const double lw0 = warp_sum(lane < NW ? f_part[lane] : 0.0);
+        const double lw1 = warp_sum(lane < NW ? f_part[NW + lane] : 0.0);
+        if (lane == 0) {
+          s_lw[slot][0] = lw0;
+          s_lw[slot][1] = lw1;
+        }
+        walk(std::integral_constant<int, 0>{});
       } else if (wid == 1) {
-        walk(O1{});
-      }
-      if (tid == 0) {
-        s_lw[slot][0] = fv[0];
-        s_lw[slot][1] = fv[1];
+        walk(std::integral_constant<int, 1>{});
       }
     }
-    team_sync();
+    __syncthreads();
     int need[2] = {s_need[slot][0], s_need[slot][1]};
     // ---- bucketed exact search for unsettled tracks ----------------------
     if (need[0] | need[1]) {
@@ -1265,6 +1289,8 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
                      (int)(p1 != g1) | (int)!known)) {
         // crossing hints for next sweep, flagged if this row searched
         const bool sr = need[0] || need[1];
+        // (the modes of the hints read at the row start: re-read here,
+        // keeping them live across the row costs registers)
         const int o0 = known ? a.hint[2 * t] : 0, o1 = known ? a.hint[2 * t + 1] : 0;
         a.hint[2 * t] = hint_encode(a, o0, p0, a.perm0, sr && known, true);
         a.hint[2 * t + 1] = hint_encode(a, o1, p1, a.perm1, sr && known, true);
@@ -1278,7 +1304,10 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
           (p0 != g0 || p1 != g1) && known && !zero)
         atomicAdd(a.miss_total, 1ull);
     }
-    team_sync();   // s_st / s_x / s_need are reused by the team's next row
+    // no barrier needed here: the next row writes s_st / s_x / s_need /
+    // s_lw and the partials only after its first barrier, which thread 0
+    // reaches once it is done with this row's
+    if constexpr (TEAM <= IMP_K5_ENDSYNC) __syncthreads();
   }
 }
 
@@ -1717,7 +1746,7 @@ bool sweep_stats() {
 
 template <int TEAM, bool WIDE>
 void launch_sweep_t(const SweepArgs& a, int sms, cudaStream_t s) {
-  void (*kern)(SweepArgs);
+  void (*kern)(const SweepArgs);
   if constexpr (TEAM == 32) kern = k_sweep_warp<32, WIDE>;
   else kern = k_sweep<TEAM, WIDE>;
   const int threads = TEAM == 32 ? 256 : TEAM;

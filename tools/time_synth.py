@@ -1,5 +1,6 @@
 """Phase-1 sweeps/s of a benchmark config's synthesis (build once, run the
 synthesis 3 times, report the best).  Usage: python tools/time_synth.py NAME [horizon]"""
+import hashlib
 import sys
 import time
 sys.path.insert(0, ".")
@@ -21,4 +22,7 @@ for _ in range(3):
     ms = ctrl.meta.get("device_ms")
     rate = it[0] / (ms[0] * 1e-3) if ms else it[0] / wall
     best = max(best or 0, rate)
-print(f"{name}: iterations {it} device_ms {ms} phase-1 sweeps/s {best:.1f}")
+dig = hashlib.sha1(ctrl.p_min.tobytes() + ctrl.p_max.tobytes() + (
+    ctrl.policy.tobytes() if ctrl.policy is not None else b"")).hexdigest()[:12]
+print(f"{name}: iterations {it} device_ms {ms} phase-1 sweeps/s {best:.1f} "
+      f"result {dig}")
