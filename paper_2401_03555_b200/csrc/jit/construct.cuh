@@ -235,6 +235,36 @@ struct NelderMead {
   // shrink decision: the same arithmetic per vertex, but done on the trip
   // every lane runs instead of in a rarely-taken branch that serialises.
   __device__ __forceinline__ void point(double* p) {
+#if IMP_NM_UNIFIED
+    // Every phase's next point is base + coef * (x - y) (clipped to the
+    // cell except for shrinks; the initial simplex: the vertex itself), so
+    // all lanes run ONE path here whatever their phase, instead of the
+    // reflection point in iterate() and the second candidate in feed()
+    // running as separate divergent blocks.  Same operands, same order,
+    // same bits (optimize.py:88, 104-117, 140-143).
+    const int ph = phase;
+    const int sv = slot(v), s0 = slot(0), sw = slot(D);
+    const bool init = ph == NM_INIT, shr = ph == NM_SHRINK;
+    const bool sec = ph == NM_SECOND;
+    const int b = shr ? s0 : (init ? sv : CEN);
+    const int x = shr || init ? sv
+                  : (sec && kind == NM_OUTSIDE ? REF
+                     : (sec && kind == NM_INSIDE ? sw : CEN));
+    const int y = shr ? s0 : (init ? sv
+                  : (sec && kind != NM_EXPAND ? CEN : sw));
+    const double coef = shr ? 0.5 : (init ? 0.0
+                        : (!sec ? 1.0 : (kind == NM_EXPAND ? 2.0 : 0.5)));
+    const int dst = shr || init ? sv : (sec ? CAND : REF);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double bv = xs(b, d);
+      double t = bv + coef * (xs(x, d) - xs(y, d));
+      t = shr ? t : imp_clip(t, lo[d], hi[d]);
+      t = init ? bv : t;
+      xs(dst, d) = t;
+      p[d] = t;
+    }
+#else
     const bool shr = phase == NM_SHRINK;
     const bool vert = phase == NM_INIT || shr;
     const int ps = vert ? slot(v) : (phase == NM_REFLECT ? REF : CAND);
@@ -249,6 +279,7 @@ struct NelderMead {
       }
       p[d] = q;
     }
+#endif
   }
 
   // stable sort, termination test, centroid and reflection point.
@@ -302,7 +333,9 @@ struct NelderMead {
       for (int vv = 1; vv < D; ++vv) s += xs(slot(vv), d);
       const double cd = imp_div_rcp(s, (double)D, 1.0 / D);
       xs(CEN, d) = cd;
+#if !IMP_NM_UNIFIED
       xs(REF, d) = imp_clip(cd + 1.0 * (cd - xs(sw, d)), lo[d], hi[d]);
+#endif
     }
     phase = NM_REFLECT;
   }
@@ -329,6 +362,7 @@ struct NelderMead {
       const double f0 = fs(slot(0)), fsw = fs(slot(D - 1)), fw = fs(sw);
       if (fr < f0 || fr >= fsw) {
         kind = fr < f0 ? NM_EXPAND : (fr < fw ? NM_OUTSIDE : NM_INSIDE);
+#if !IMP_NM_UNIFIED
         const double coef = kind == NM_EXPAND ? 2.0 : 0.5;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
@@ -337,6 +371,7 @@ struct NelderMead {
                              : (kind == NM_OUTSIDE ? xs(REF, d) - cd : w - cd);
           xs(CAND, d) = imp_clip(cd + coef * dir, lo[d], hi[d]);
         }
+#endif
         phase = NM_SECOND;
       } else {
         replace = true;          // from REF, value fr
