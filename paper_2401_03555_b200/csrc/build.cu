@@ -157,8 +157,11 @@ std::string config_header(const imp_build_desc* d) {
   o << "#define IMP_NDTR_LEGACY " << (leg ? atoi(leg) : 0) << "\n";
   const char* ftab = getenv("IMPACT_NDTR_FAST_TABLE");
   o << "#define IMP_NDTR_FAST_TABLE " << (ftab ? atoi(ftab) : 0) << "\n";
+  // Nelder-Mead next point on one shared path for every phase (same bits;
+  // vehicle3d refine 12.73 -> 12.48 s, room5d 19.39 -> 18.49 s:
+  // profiles/r02/k_refine_nm_unified_ab.txt)
   const char* nmu = getenv("IMPACT_NM_UNIFIED");
-  o << "#define IMP_NM_UNIFIED " << (nmu ? atoi(nmu) : 0) << "\n";
+  o << "#define IMP_NM_UNIFIED " << (nmu ? atoi(nmu) : 1) << "\n";
   const char* batch = getenv("IMPACT_REFINE_BATCH");
   o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 4) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
