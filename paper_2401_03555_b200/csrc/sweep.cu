@@ -879,16 +879,6 @@ __global__ void __launch_bounds__(256, IMP_K5_TPSM / 256)
         if (c1 != HINT_COL) { r.load(a, c1); g1 = r.r1(); } else g1 = a.n;
       }
     }
-    // rows that searched last sweep (or have no hint) will likely search
-    // again: pass A fills the first search level's histogram on the way
-    // (the same exact integer adds, so the search result is unchanged)
-    const bool spec = false;
-    const int shs = max(0, a.nbits - SH::LOGB);
-    if (spec) {
-      team_sync();   // the previous row's histogram adds are complete
-      for (int q = tid; q < SH::HIST; q += TEAM) hist[q] = 0ull;
-      team_sync();
-    }
     // ---- pass A ----------------------------------------------------------
     // fv: lw0 lw1 | F0 F1 (sum h*w, rank < g) | C0 C1 (sum h, rank < g),
     // all float in the canonical order; heads ranked in [g - W, g + W) are
@@ -909,11 +899,6 @@ __global__ void __launch_bounds__(256, IMP_K5_TPSM / 256)
           const unsigned d0 = (unsigned)(r0 - wb0), d1 = (unsigned)(r1 - wb1);
           if (d0 < 2 * W) win[d0] = h;
           if (d1 < 2 * W) win[2 * W + d1] = h;
-          if (spec) {
-            const Fix x = to_fix(h);
-            hist_add(hist + ((unsigned)r0 >> shs) * 2, x);
-            hist_add(hist + (SH::B + ((unsigned)r1 >> shs)) * 2, x);
-          }
         });
     team_sum_pass_a<TEAM>(fv, f_part, s_win[slot][par ^ 1], SH::WIN);
     int P[2] = {g0, g1};
@@ -975,7 +960,7 @@ __global__ void __launch_bounds__(256, IMP_K5_TPSM / 256)
       }
       team_sync();
       if (need[0] == 2 || need[1] == 2)
-        search_levels<TEAM, WIDE>(a, tid, row, beg, m, s, st, hist, spec);
+        search_levels<TEAM, WIDE>(a, tid, row, beg, m, s, st, hist, false);
       // ---- pass F: the canonical float sums below the new crossings -----
       // (same per-lane order and team tree as pass A, so a row's bits do not
       // depend on which path found P)
