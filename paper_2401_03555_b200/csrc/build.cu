@@ -162,6 +162,14 @@ std::string config_header(const imp_build_desc* d) {
   // profiles/r02/k_refine_nm_unified_ab.txt)
   const char* nmu = getenv("IMPACT_NM_UNIFIED");
   o << "#define IMP_NM_UNIFIED " << (nmu ? atoi(nmu) : 1) << "\n";
+  // exact objective: each dimension's factor formed as soon as its two
+  // CDFs are known, no cdf array in local memory (same bits; vehicle3d
+  // refine 12.48 -> 12.25 s, room5d 18.49 -> 17.82 s:
+  // profiles/r02/k_refine_obj_fused_ab.txt)
+  const char* ofu = getenv("IMPACT_OBJ_FUSED");
+  o << "#define IMP_OBJ_FUSED " << (ofu ? atoi(ofu) : 1) << "\n";
+  // (IMPACT_REFINE_CARVEOUT: the k_refine shared-memory carve-out hint, an
+  // experiment knob; the driver's default is the fastest measured)
   const char* batch = getenv("IMPACT_REFINE_BATCH");
   o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 4) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
@@ -597,6 +605,9 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
       if (smem3 > 48 * 1024)
         IMP_CUDA(cudaFuncSetAttribute(
             rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+      if (const char* co = getenv("IMPACT_REFINE_CARVEOUT"))   // experiment
+        IMP_CUDA(cudaFuncSetAttribute(
+            rfn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co)));
       int per_sm = 0;
       IMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rfn,
                                                              block3, smem3));

@@ -1205,6 +1205,26 @@ __device__ __forceinline__ double imp_box_objective(const BuildParams& P,
 #pragma unroll
   for (int j = 0; j < 2 * IMP_N; j += IMP_NDTR_CHUNK)
     imp_ndtr_batch_x<IMP_NDTR_CHUNK>(arg + j, cdf + j, ndtr_tab, exp_tab);
+#elif IMP_OBJ_FUSED
+  // each dimension's factor as soon as its two CDFs are known: no cdf
+  // array in local memory, the same products in the same order
+  double pr = 1.0, c_hi = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < 2 * IMP_N; ++j) {
+    double c;
+#if IMP_OBJ_FUSED == 2   // the argument by a select chain, not local memory
+    double aj = arg[0];
+#pragma unroll
+    for (int q = 1; q < 2 * IMP_N; ++q) aj = j == q ? arg[q] : aj;
+    imp_ndtr_batch_x<1>(&aj, &c, ndtr_tab, exp_tab);
+#else
+    imp_ndtr_batch_x<1>(arg + j, &c, ndtr_tab, exp_tab);
+#endif
+    if (j & 1) pr *= c_hi - c;
+    else c_hi = c;
+  }
+  (void)cdf;
+  return I.sgn ? pr * -1.0 : pr;
 #else
 #pragma unroll 1
   for (int j = 0; j < 2 * IMP_N; j += IMP_NDTR_CHUNK)
