@@ -171,7 +171,9 @@ std::string config_header(const imp_build_desc* d) {
   // (IMPACT_REFINE_CARVEOUT: the k_refine shared-memory carve-out hint, an
   // experiment knob; the driver's default is the fastest measured)
   const char* batch = getenv("IMPACT_REFINE_BATCH");
-  o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 4) << "\n";
+  // k_refine work grab: 8 boxes per atomic (fewer binary-search seeks;
+  // vehicle3d 12.25 -> 12.11 s, profiles/r02/k_refine_batch_ab.txt)
+  o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 16) << "\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
   for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->n_deps[q];
   o << "};\n__device__ constexpr int kDeps[IMP_N][IMP_N] = {";
