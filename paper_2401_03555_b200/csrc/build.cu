@@ -141,8 +141,11 @@ std::string config_header(const imp_build_desc* d) {
   // tuning knobs (environment overrides for experiments)
   const char* minb = getenv("IMPACT_REFINE_MINB");
   // defaults measured on the full vehicle3d / room5d builds (subsets mislead)
+  // (n = 5: shared memory admits 3 blocks of 128 per SM, so a register
+  // cap for 4 only adds spills -- room5d refine 17.86 -> 17.27 s with 3;
+  // n >= 6: 2 blocks fit.  profiles/r02/k_refine_minb_ab.txt)
   o << "#define IMP_REFINE_MINB "
-    << (minb ? atoi(minb) : (d->n <= 4 ? 5 : d->n <= 8 ? 4 : 2))
+    << (minb ? atoi(minb) : (d->n <= 4 ? 5 : d->n == 5 ? 3 : 2))
     << "\n";
   const char* ch = getenv("IMPACT_NDTR_CHUNK");
   // CDF chains interleaved per step: fast objective 2 (full vehicle3d
