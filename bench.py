@@ -199,7 +199,9 @@ def cpu_sweep_baseline(name, n_rows, n_s, rows_sample=4, tile=2000,
             "sample": f"oracle RowsSolver.values twin sweep on {len(rows)} "
                       f"real rows of {name} (oracle construction) tiled to "
                       f"{nrows} rows, {dt * 1e3:.0f} ms, extrapolated "
-                      f"linearly to {n_rows} rows; 1 process"}
+                      f"linearly to {n_rows} rows; 1 process, as the "
+                      f"reference iterates (its process pool serves only "
+                      f"the construction, abstraction.py:571-592)"}
 
 
 # --- the GPU step ---------------------------------------------------------------
