@@ -3,7 +3,7 @@
 * world 1 over NCCL (one process): sharded.synthesize -- device loop, NCCL
   in-place all-gather and all-reduce, CUDA graphs of 16 iterations -- equals
   the single-GPU synthesis bit for bit, with graphs and without;
-* three shards of a cost-balanced table driven from one process, the
+* 2 / 3 / 4 / 8 shards of a cost-balanced table driven from one process, the
   collectives done by copies between the shards' packed buffers (no rank
   waits on another): the packed layout, uneven shards and the device
   control step give the single-GPU result bit for bit.
@@ -108,8 +108,9 @@ def _drive(engines, spec, lp, u_obj, eps, horizon, table, fixed=None):
     return res
 
 
+@pytest.mark.parametrize("n_shards", (2, 3, 4, 8))
 @pytest.mark.parametrize("name", NAMES)
-def test_three_balanced_shards_equal_single_gpu(name):
+def test_balanced_shards_equal_single_gpu(name, n_shards):
     g = G.load("full_" + name)
     cfg = G.config_of(g)
     labels = cfg.labels()
@@ -118,9 +119,9 @@ def test_three_balanced_shards_equal_single_gpu(name):
     cost = state_costs(cfg.dynamics, cfg.noise, cfg.spaces, labels,
                        cfg.abstraction_options())
     assert len(cost) == full.n_s and np.all(cost >= 1)
-    table = sharded.balanced_shards(cost, 3)
+    table = sharded.balanced_shards(cost, n_shards)
     engines = []
-    for r in range(3):
+    for r in range(n_shards):
         sh = build_abstraction(cfg.dynamics, cfg.noise, cfg.spaces, labels,
                                cfg.abstraction_options(),
                                k_range=(int(table[r]),
