@@ -177,6 +177,21 @@ std::string config_header(const imp_build_desc* d) {
   // k_refine work grab: 8 boxes per atomic (fewer binary-search seeks;
   // vehicle3d 12.25 -> 12.11 s, profiles/r02/k_refine_batch_ab.txt)
   o << "#define IMP_REFINE_BATCH " << (batch ? atoi(batch) : 16) << "\n";
+  // the lattice shape as compile-time constants: index arithmetic by
+  // multiply-shift instead of the integer-division sequence
+  o << "__device__ constexpr int kCounts[IMP_N] = {";
+  for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->counts[q];
+  o << "};\n__device__ constexpr int kStrides[IMP_N] = {";   // row-major
+  {
+    std::vector<long long> st(d->n);
+    long long t = 1;
+    for (int q = d->n - 1; q >= 0; --q) {
+      st[q] = t;
+      t *= d->counts[q];
+    }
+    for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << st[q];
+  }
+  o << "};\n";
   o << "__device__ constexpr int kNDeps[IMP_N] = {";
   for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->n_deps[q];
   o << "};\n__device__ constexpr int kDeps[IMP_N][IMP_N] = {";

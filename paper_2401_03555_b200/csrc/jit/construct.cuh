@@ -406,6 +406,29 @@ struct NelderMead {
 };
 
 
+// Division of 0 <= n < 2^31 by a run-time divisor d >= 1 fixed per row
+// (the pruned box's extents): q = umulhi(n, mul) >> shr with mul =
+// ceil(2^p / d), p = 31 + ceil(log2 d) -- exact for every such n, two
+// instructions instead of the integer-division sequence.
+struct ImpFastDiv {
+  unsigned mul;   // 0: d == 1
+  int shr;
+};
+__device__ __forceinline__ ImpFastDiv imp_fastdiv(int d) {
+  ImpFastDiv f{0u, 0};
+  if (d > 1) {
+    const int l = 32 - __clz(d - 1);
+    const int p = 31 + l;
+    f.mul = (unsigned)(((1ull << p) + (unsigned long long)d - 1) /
+                       (unsigned long long)d);
+    f.shr = p - 32;
+  }
+  return f;
+}
+__device__ __forceinline__ int imp_fdiv(int n, ImpFastDiv f) {
+  return f.mul ? (int)(__umulhi((unsigned)n, f.mul) >> f.shr) : n;
+}
+
 __device__ __forceinline__ void imp_flag_nonfinite(const BuildParams& P,
                                                    long long row) {
   atomicMin(P.err, (unsigned long long)row);
@@ -501,7 +524,7 @@ __device__ long long imp_mean_task(const BuildParams& P, long long r, int sgn,
 __device__ __forceinline__ long long imp_sep_key(const BuildParams& P, int d,
                                                  int c, int j, int i) {
   long long off = 0;
-  for (int e = 0; e < d; ++e) off += (long long)P.counts[e] * P.n_u * P.n_w;
+  for (int e = 0; e < d; ++e) off += (long long)kCounts[e] * P.n_u * P.n_w;
   return off + ((long long)c * P.n_u + j) * P.n_w + i;
 }
 
@@ -509,8 +532,8 @@ __device__ __forceinline__ long long imp_sep_tab(const BuildParams& P, int d,
                                                  int c, int j, int i) {
   long long off = 0;
   for (int e = 0; e < d; ++e)
-    off += 2ll * P.counts[e] * P.counts[e] * P.n_u * P.n_w;
-  return off + (((long long)c * P.n_u + j) * P.n_w + i) * 2 * P.counts[d];
+    off += 2ll * kCounts[e] * kCounts[e] * P.n_u * P.n_w;
+  return off + (((long long)c * P.n_u + j) * P.n_w + i) * 2 * kCounts[d];
 }
 
 template <int DI>
@@ -532,8 +555,8 @@ extern "C" __global__ void __launch_bounds__(IMP_MEAN_BLOCK)
   constexpr int S = IMP_MEAN_BLOCK;
   long long nkeys = 0, nbins = 0;
   for (int e = 0; e < IMP_N; ++e) {
-    nkeys += (long long)P.counts[e] * P.n_u * P.n_w;
-    nbins += (long long)P.counts[e] * P.counts[e] * P.n_u * P.n_w;
+    nkeys += (long long)kCounts[e] * P.n_u * P.n_w;
+    nbins += (long long)kCounts[e] * kCounts[e] * P.n_u * P.n_w;
   }
   unsigned long long ev = 0;
   const long long ntask = P.write ? nbins : 2 * nkeys;
@@ -543,18 +566,18 @@ extern "C" __global__ void __launch_bounds__(IMP_MEAN_BLOCK)
     int d = 0, coord0 = 0;
     long long rem = P.write ? t : t >> 1, koff = 0;
     for (;;) {
-      const long long kd = (long long)P.counts[d] * P.n_u * P.n_w;
-      const long long per = P.write ? kd * P.counts[d] : kd;
+      const long long kd = (long long)kCounts[d] * P.n_u * P.n_w;
+      const long long per = P.write ? kd * kCounts[d] : kd;
       if (rem < per) break;
       rem -= per;
       koff += kd;
-      coord0 += P.counts[d];
+      coord0 += kCounts[d];
       ++d;
     }
     int q = 0;
     if (P.write) {
-      q = (int)(rem % P.counts[d]);
-      rem /= P.counts[d];
+      q = (int)(rem % kCounts[d]);
+      rem /= kCounts[d];
     }
     const int i = (int)(rem % P.n_w);
     const long long rest = rem / P.n_w;
@@ -665,12 +688,13 @@ extern "C" __global__ void k_outer(BuildParams P) {
   __shared__ double red[32];
   __shared__ int wsum[32];
   __shared__ int s_blo[IMP_N], s_bext[IMP_N];
+  __shared__ ImpFastDiv s_fdiv[IMP_N];
   __shared__ int s_lo[IMP_N], s_hi[IMP_N];
   __shared__ unsigned long long s_pm[IMP_N];
   __shared__ double s_ml[IMP_N], s_mh[IMP_N];
   __shared__ double s_cov[3 * IMP_N];
   int nbins = 0;
-  for (int d = 0; d < IMP_N; ++d) nbins += P.counts[d];
+  for (int d = 0; d < IMP_N; ++d) nbins += kCounts[d];
   double* gmin = smem;
   double* gmax = smem + nbins;
 
@@ -681,7 +705,7 @@ extern "C" __global__ void k_outer(BuildParams P) {
     if (threadIdx.x < IMP_N) {
       if (P.sep) {
         const int d = threadIdx.x;
-        const int c = (rflat / P.strides[d]) % P.counts[d];
+        const int c = (rflat / kStrides[d]) % kCounts[d];
         const long long kk = imp_sep_key(P, d, c, rj, ri);
         s_ml[d] = P.sep_mr[2 * kk];
         s_mh[d] = P.sep_mr[2 * kk + 1];
@@ -694,8 +718,8 @@ extern "C" __global__ void k_outer(BuildParams P) {
     if (P.sep) {   // separable: gather this row's tables (k_sep_tables)
       int d = 0, base = 0;
       for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-        while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
-        const int c = (rflat / P.strides[d]) % P.counts[d];
+        while (b >= base + kCounts[d]) { base += kCounts[d]; ++d; }
+        const int c = (rflat / kStrides[d]) % kCounts[d];
         const double* tab = P.sep_tab + imp_sep_tab(P, d, c, rj, ri);
         const int q = b - base;
         gmin[b] = tab[2 * q];
@@ -710,7 +734,7 @@ extern "C" __global__ void k_outer(BuildParams P) {
     if (!IMP_MC && !P.sep) {
       int d = 0, base = 0;
       for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-        while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
+        while (b >= base + kCounts[d]) { base += kCounts[d]; ++d; }
         const int q = b - base;
         const double* e = P.edges + P.edge_off[d];
         const double s = P.sigma[d], ml = s_ml[d], mh = s_mh[d];
@@ -736,20 +760,20 @@ extern "C" __global__ void k_outer(BuildParams P) {
     if (IMP_MC) {
       if (threadIdx.x < IMP_N) {
         s_blo[threadIdx.x] = 0;
-        s_bext[threadIdx.x] = P.counts[threadIdx.x];
+        s_bext[threadIdx.x] = kCounts[threadIdx.x];
       }
       __syncthreads();
     } else {
       if (threadIdx.x < IMP_N) {
         s_pm[threadIdx.x] = 0ull;
-        s_lo[threadIdx.x] = P.counts[threadIdx.x];
+        s_lo[threadIdx.x] = kCounts[threadIdx.x];
         s_hi[threadIdx.x] = -1;
       }
       __syncthreads();
       {   // pm_d = max_q gmax_d[q] (gmax >= 0: bit order = value order)
         int d = 0, base = 0;
         for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-          while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
+          while (b >= base + kCounts[d]) { base += kCounts[d]; ++d; }
           const double gm = gmax[b] > 0.0 ? gmax[b] : 0.0;
           atomicMax(&s_pm[d], (unsigned long long)__double_as_longlong(gm));
           d = 0;
@@ -760,7 +784,7 @@ extern "C" __global__ void k_outer(BuildParams P) {
       {   // superlevel interval of gmax_d above cutoff / prod_{e != d} pm_e
         int d = 0, base = 0;
         for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-          while (b >= base + P.counts[d]) { base += P.counts[d]; ++d; }
+          while (b >= base + kCounts[d]) { base += kCounts[d]; ++d; }
           double rest = 1.0;
           for (int e = 0; e < IMP_N; ++e)
             if (e != d) rest *= __longlong_as_double((long long)s_pm[e]);
@@ -781,6 +805,8 @@ extern "C" __global__ void k_outer(BuildParams P) {
       }
       __syncthreads();
     }
+    if (threadIdx.x < IMP_N) s_fdiv[threadIdx.x] = imp_fastdiv(s_bext[threadIdx.x]);
+    __syncthreads();
     int box = 1;   // < 2^31: a sub-box of the state lattice
     for (int d = 0; d < IMP_N; ++d) box *= s_bext[d];
 
@@ -797,10 +823,11 @@ extern "C" __global__ void k_outer(BuildParams P) {
         int bidx[IMP_N];
 #pragma unroll
         for (int d = IMP_N - 1; d >= 0; --d) {
-          const int b = s_blo[d] + (int)(rem % s_bext[d]);
-          rem /= s_bext[d];
+          const int qd = imp_fdiv(rem, s_fdiv[d]);
+          const int b = s_blo[d] + (rem - qd * s_bext[d]);
+          rem = qd;
           bidx[d] = b;
-          flat += b * P.strides[d];
+          flat += b * kStrides[d];
         }
         pos = P.label ? P.label[flat] : flat;
         if (pos >= 0) {
@@ -810,7 +837,7 @@ extern "C" __global__ void k_outer(BuildParams P) {
             const double a = gmax[base + bidx[d]], c = gmin[base + bidx[d]];
             tmax = d == 0 ? a : tmax * a;
             tmin = d == 0 ? c : tmin * c;
-            base += P.counts[d];
+            base += kCounts[d];
           }
           live = IMP_MC ? 1 : tmax > P.cutoff;
         }
@@ -845,11 +872,11 @@ extern "C" __global__ void k_outer(BuildParams P) {
           int base = 0;
 #pragma unroll
           for (int d = 0; d < IMP_N; ++d) {
-            const int b = (flat / P.strides[d]) % P.counts[d];
+            const int b = (flat / kStrides[d]) % kCounts[d];
             const double a = gmax[base + b], c = gmin[base + b];
             tmax = d == 0 ? a : tmax * a;
             tmin = d == 0 ? c : tmin * c;
-            base += P.counts[d];
+            base += kCounts[d];
           }
           live = IMP_MC ? 1 : tmax > P.cutoff;
           if (kind == 0) { rs[0] += tmin; rs[1] += tmax; }
@@ -911,6 +938,8 @@ extern "C" __global__ void k_outer(BuildParams P) {
 // fixed xor tree.  P.write = 0: counts; 1: CSR values, r / a sums, leak.
 extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
   const int lane = threadIdx.x & 31;
+  __shared__ ImpFastDiv s_fd[8][IMP_N];   // per warp: the box extents'
+  ImpFastDiv* fd = s_fd[threadIdx.x >> 5];
   const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long r = w0; r < P.n_rows; r += nw) {
@@ -922,12 +951,12 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
     int cnt_d[IMP_N];
 #pragma unroll
     for (int d = 0; d < IMP_N; ++d) {
-      const int c = (rflat / P.strides[d]) % P.counts[d];
+      const int c = (rflat / kStrides[d]) % kCounts[d];
       tab[d] = P.sep_tab + imp_sep_tab(P, d, c, rj, ri);
       const long long kk = imp_sep_key(P, d, c, rj, ri);
       ml[d] = P.sep_mr[2 * kk];
       mh[d] = P.sep_mr[2 * kk + 1];
-      cnt_d[d] = P.counts[d];
+      cnt_d[d] = kCounts[d];
     }
     // pm_d = max gmax_d (exact), then the superlevel index interval
     double pm[IMP_N];
@@ -962,6 +991,11 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
       box *= bext[d];
     }
     // safe destinations
+    __syncwarp();
+#pragma unroll
+    for (int d = 0; d < IMP_N; ++d)
+      if (lane == d) fd[d] = imp_fastdiv(bext[d]);
+    __syncwarp();
     long long out = P.write ? P.row_ptr[r] : 0;
     long long cnt = 0;
     for (int q0 = 0; q0 < box; q0 += 32) {
@@ -973,10 +1007,11 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
         int bidx[IMP_N];
 #pragma unroll
         for (int d = IMP_N - 1; d >= 0; --d) {
-          const int b = blo[d] + rem % bext[d];
-          rem /= bext[d];
+          const int qd = imp_fdiv(rem, fd[d]);
+          const int b = blo[d] + (rem - qd * bext[d]);
+          rem = qd;
           bidx[d] = b;
-          flat += b * P.strides[d];
+          flat += b * kStrides[d];
         }
         pos = P.label ? P.label[flat] : flat;
         if (pos >= 0) {
@@ -1012,7 +1047,7 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
         double tmin = 0.0, tmax = 0.0;
 #pragma unroll
         for (int d = 0; d < IMP_N; ++d) {
-          const int bb = (flat / P.strides[d]) % P.counts[d];
+          const int bb = (flat / kStrides[d]) % kCounts[d];
           const double a = tab[d][2 * bb + 1], c = tab[d][2 * bb];
           tmax = d == 0 ? a : tmax * a;
           tmin = d == 0 ? c : tmin * c;
