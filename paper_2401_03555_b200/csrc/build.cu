@@ -181,7 +181,19 @@ std::string config_header(const imp_build_desc* d) {
   // multiply-shift instead of the integer-division sequence
   o << "__device__ constexpr int kCounts[IMP_N] = {";
   for (int q = 0; q < d->n; ++q) o << (q ? ", " : "") << d->counts[q];
-  o << "};\n__device__ constexpr int kStrides[IMP_N] = {";   // row-major
+  o << "};\n";
+  // a separable row's 1-D tables ({min, max} per coordinate of every
+  // dimension): offsets and size, for staging them per warp in k_outer_sep
+  {
+    int tot = 0;
+    o << "__device__ constexpr int kTabOff[IMP_N] = {";
+    for (int q = 0; q < d->n; ++q) {
+      o << (q ? ", " : "") << tot;
+      tot += 2 * d->counts[q];
+    }
+    o << "};\n#define IMP_TAB_DOUBLES " << tot << "\n";
+  }
+  o << "__device__ constexpr int kStrides[IMP_N] = {";   // row-major
   {
     std::vector<long long> st(d->n);
     long long t = 1;

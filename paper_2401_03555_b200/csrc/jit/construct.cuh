@@ -940,6 +940,10 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
   const int lane = threadIdx.x & 31;
   __shared__ ImpFastDiv s_fd[8][IMP_N];   // per warp: the box extents'
   ImpFastDiv* fd = s_fd[threadIdx.x >> 5];
+  // per warp: the row's 1-D tables (small lattices; else read in place)
+  constexpr bool STAGE = IMP_TAB_DOUBLES <= 256;
+  __shared__ double s_tab[8][STAGE ? IMP_TAB_DOUBLES : 1];
+  double* stab = s_tab[threadIdx.x >> 5];
   const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long r = w0; r < P.n_rows; r += nw) {
@@ -949,6 +953,7 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
     const double* tab[IMP_N];
     double ml[IMP_N], mh[IMP_N];
     int cnt_d[IMP_N];
+    if (STAGE) __syncwarp();   // the previous row's reads are done
 #pragma unroll
     for (int d = 0; d < IMP_N; ++d) {
       const int c = (rflat / kStrides[d]) % kCounts[d];
@@ -957,13 +962,22 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
       ml[d] = P.sep_mr[2 * kk];
       mh[d] = P.sep_mr[2 * kk + 1];
       cnt_d[d] = kCounts[d];
+      if (STAGE) {
+        for (int q = lane; q < 2 * kCounts[d]; q += 32)
+          stab[kTabOff[d] + q] = tab[d][q];
+      }
     }
+    if (STAGE) __syncwarp();
+    // table value idx of dimension d (shared-memory copy when staged)
+    auto tv = [&](int d, int idx) -> double {
+      return STAGE ? stab[kTabOff[d] + idx] : tab[d][idx];
+    };
     // pm_d = max gmax_d (exact), then the superlevel index interval
     double pm[IMP_N];
 #pragma unroll
     for (int d = 0; d < IMP_N; ++d) {
       double m = 0.0;
-      for (int q = lane; q < cnt_d[d]; q += 32) m = fmax(m, tab[d][2 * q + 1]);
+      for (int q = lane; q < cnt_d[d]; q += 32) m = fmax(m, tv(d, 2 * q + 1));
       for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
       pm[d] = m;
     }
@@ -980,7 +994,7 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
       for (int q0 = 0; q0 < cnt_d[d]; q0 += 32) {
         const int q = q0 + lane;
         const unsigned b = __ballot_sync(0xffffffffu,
-                                         q < cnt_d[d] && tab[d][2 * q + 1] > thr);
+                                         q < cnt_d[d] && tv(d, 2 * q + 1) > thr);
         if (b) {
           lo = min(lo, q0 + __ffs(b) - 1);
           hi = q0 + 31 - __clz(b);
@@ -1017,7 +1031,7 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
         if (pos >= 0) {
 #pragma unroll
           for (int d = 0; d < IMP_N; ++d) {
-            const double a = tab[d][2 * bidx[d] + 1], c = tab[d][2 * bidx[d]];
+            const double a = tv(d, 2 * bidx[d] + 1), c = tv(d, 2 * bidx[d]);
             tmax = d == 0 ? a : tmax * a;
             tmin = d == 0 ? c : tmin * c;
           }
@@ -1048,7 +1062,7 @@ extern "C" __global__ void __launch_bounds__(256) k_outer_sep(BuildParams P) {
 #pragma unroll
         for (int d = 0; d < IMP_N; ++d) {
           const int bb = (flat / kStrides[d]) % kCounts[d];
-          const double a = tab[d][2 * bb + 1], c = tab[d][2 * bb];
+          const double a = tv(d, 2 * bb + 1), c = tv(d, 2 * bb);
           tmax = d == 0 ? a : tmax * a;
           tmin = d == 0 ? c : tmin * c;
         }
