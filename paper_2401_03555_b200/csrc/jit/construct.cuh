@@ -1610,7 +1610,8 @@ extern "C" __global__ void k_assemble(BuildParams P) {
     double smin = 0.0, smax = 0.0;
     unsigned live = 0;   // t_max > cutoff (the reference's sparsity log)
     for (long long q = b + lane; q < e; q += 32) {
-      double hv = P.hi[q], lv = P.lo[q];
+      const double hv0 = P.hi[q], lv0 = P.lo[q];
+      double hv = hv0, lv = lv0;
       if (IMP_MC) {     // abstraction.py:518-522
         if (hv <= P.cutoff) lv = hv = 0.0;
         lv = fmin(lv, hv);
@@ -1619,8 +1620,10 @@ extern "C" __global__ void k_assemble(BuildParams P) {
       double lo = imp_clip(lv, 0.0, 1.0);
       if (P.low_cost && hi <= P.cutoff) lo = 0.0;
       lo = fmin(lo, hi);
-      P.lo[q] = lo;
-      P.hi[q] = hi;
+      // store only what changed (bitwise): the writers already clip and
+      // order most entries, so this halves the kernel's HBM traffic
+      if (__double_as_longlong(lo) != __double_as_longlong(lv0)) P.lo[q] = lo;
+      if (__double_as_longlong(hi) != __double_as_longlong(hv0)) P.hi[q] = hi;
       smin += lo;
       smax += hi;
       live += hi > P.cutoff;
