@@ -353,6 +353,26 @@ def run_b200(args):
                            "2 flops/DFMA; MEASURED_PEAKS.json has no FP64 "
                            "entry and B200_PROFILING.md no FP64 fallback)",
         }
+    elif top == "mean_ranges" and report.nm_evals_mean:
+        # mean ranges dominate (bas7d: the lattice probabilities vanish
+        # under the cutoff, so there is almost nothing to refine or write):
+        # Nelder-Mead over each dynamics component, FP64 flops = evals x
+        # (the component's share of F_dyn)
+        f_comp = max(_dyn_flops(cfg.dynamics), 1) / cfg.dynamics.dims[0]
+        mean_tflops = report.nm_evals_mean * f_comp / \
+            (report.ms_mean_ranges * 1e-3) / 1e12
+        roofline = {
+            "kernel": "k_mean_ranges", "bound": "fp64",
+            "achieved": mean_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": mean_tflops / fp64_peak, "traffic": None,
+            "flops_per_eval": f_comp,
+            "evals_per_step": report.nm_evals_mean,
+            "kernel_ms": report.ms_mean_ranges,
+            "peak_source": "measured DFMA microbenchmark (imp_fp64_peak)",
+            "note": "one dynamics component per evaluation: the kernel is "
+                    "Nelder-Mead bookkeeping (sort, centroid, accept) bound, "
+                    "not FP64-throughput bound",
+        }
     else:
         out_bytes = nnz * 20 + rows_total * (8 + 48)
         gbs = out_bytes / (report.ms_outer * 1e-3) / 1e9

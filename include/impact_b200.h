@@ -170,12 +170,15 @@ typedef struct imp_build_stats {
   double ms_total, ms_mean_ranges, ms_outer, ms_refine, ms_assemble;
   int64_t nnz;
   int64_t nm_instances;
-  int64_t nm_evals;          /* objective evaluations (all NM instances)    */
+  int64_t nm_evals;          /* refinement objective evaluations (k_refine,
+                                shared initial simplices included)        */
   int64_t nm_lane_slots;     /* refine-loop lane slots (warp trips x 32):
                                 nm_evals / nm_lane_slots = SIMT efficiency */
   int64_t nm_evals_shared;   /* of nm_evals: initial-simplex values a max
                                 run took from its min run (not evaluated) */
   int64_t nnz_live;          /* stored entries with t_max > zero_cutoff   */
+  int64_t nm_evals_mean;     /* mean-range NM evaluations (k_mean_ranges /
+                                k_sep_tables: one dynamics component each) */
 } imp_build_stats;
 
 int imp_build(const imp_build_desc* desc, imp_imdp** out,

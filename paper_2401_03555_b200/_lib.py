@@ -62,7 +62,7 @@ class BuildStats(ctypes.Structure):
                 ("ms_assemble", c_dbl), ("nnz", c_i64),
                 ("nm_instances", c_i64), ("nm_evals", c_i64),
                 ("nm_lane_slots", c_i64), ("nm_evals_shared", c_i64),
-                ("nnz_live", c_i64)]
+                ("nnz_live", c_i64), ("nm_evals_mean", c_i64)]
 
 
 class PhaseDesc(ctypes.Structure):

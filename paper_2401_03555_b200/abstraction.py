@@ -257,6 +257,7 @@ class BuildReport:
     entries: int          # rows * n_s: the reference's `d`
     nm_evals_shared: int = 0   # of nm_evals: initial-simplex values reused
     nnz_live: int = 0          # stored entries with t_max > zero_cutoff
+    nm_evals_mean: int = 0     # mean-range NM evaluations (one f_d each)
 
 
 def exact_default():
@@ -295,7 +296,7 @@ def build_abstraction(dyn, noise, spaces, labels, opts=None,
         stats.ms_total, stats.ms_mean_ranges, stats.ms_outer,
         stats.ms_refine, stats.ms_assemble, stats.nnz, stats.nm_instances,
         stats.nm_evals, stats.nm_lane_slots, rows, rows * desc.n_s,
-        stats.nm_evals_shared, stats.nnz_live)
+        stats.nm_evals_shared, stats.nnz_live, stats.nm_evals_mean)
     # the reference's build log line (abstraction.py:596-598)
     entries = rows * desc.n_s
     frac_zero = 1.0 - stats.nnz_live / entries if entries else 1.0

@@ -421,10 +421,10 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     // [0] objective evals (the reference's count), [1] refine lane slots,
     // [2] refine work counter, [3] evals saved by shared initial simplices,
     // [4] stored entries with t_max > zero_cutoff (k_assemble)
-    DevBuf<long long> evals(5);
+    DevBuf<long long> evals(6);
     IMP_CUDA(cudaMemsetAsync(err.ptr, 0xff, 3 * sizeof(unsigned long long), s));
     IMP_CUDA(cudaMemsetAsync(err_val.ptr, 0, 3 * sizeof(double), s));
-    IMP_CUDA(cudaMemsetAsync(evals.ptr, 0, 5 * sizeof(long long), s));
+    IMP_CUDA(cudaMemsetAsync(evals.ptr, 0, 6 * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(tcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(xcnt.ptr, 0, (n_rows + 1) * sizeof(long long), s));
     IMP_CUDA(cudaMemsetAsync(raw.ptr, 0, (n_rows * 6 + 1) * sizeof(double), s));
@@ -669,7 +669,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
 
     unsigned long long herr[3];
     double hval[3];
-    long long hev = 0, hslots = 0, hshared = 0, hlive = 0;
+    long long hev = 0, hslots = 0, hshared = 0, hlive = 0, hmean = 0;
     IMP_CUDA(cudaMemcpy(herr, err.ptr, sizeof(herr), cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(hval, err_val.ptr, sizeof(hval), cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(&hev, evals.ptr, sizeof(hev), cudaMemcpyDeviceToHost));
@@ -678,6 +678,8 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
     IMP_CUDA(cudaMemcpy(&hshared, evals.ptr + 3, sizeof(hshared),
                         cudaMemcpyDeviceToHost));
     IMP_CUDA(cudaMemcpy(&hlive, evals.ptr + 4, sizeof(hlive),
+                        cudaMemcpyDeviceToHost));
+    IMP_CUDA(cudaMemcpy(&hmean, evals.ptr + 5, sizeof(hmean),
                         cudaMemcpyDeviceToHost));
     const long long row0 = (long long)d->k_begin * d->n_u * d->n_w;
     if (herr[0] != ~0ull) {
@@ -712,6 +714,7 @@ extern "C" int imp_build(const imp_build_desc* d, imp_imdp** out,
       stats->nm_lane_slots = hslots;
       stats->nm_evals_shared = hshared;
       stats->nnz_live = hlive;
+      stats->nm_evals_mean = hmean;
     }
     *out = h;
   });

@@ -86,7 +86,10 @@ struct BuildParams {
                               //              leak_min leak_max
   // stage 3
   long long n_items;          // nnz + n_aux + n_rows
-  long long* evals;           // total objective evaluations (atomic)
+  long long* evals;           // counters (atomic): [0] refinement evals,
+                              // [1] lane slots, [2] work cursor, [3] shared
+                              // simplex values, [4] live entries, [5]
+                              // mean-range evals
   // stage 4
   double* r_min;
   double* r_max;
@@ -609,7 +612,7 @@ extern "C" __global__ void __launch_bounds__(IMP_MEAN_BLOCK)
       tab[2 * q + 1] = top;
     }
   }
-  if (ev) atomicAdd((unsigned long long*)P.evals, ev);
+  if (ev) atomicAdd((unsigned long long*)P.evals + 5, ev);   // mean-range NM
 }
 
 template <int DI>
@@ -636,7 +639,7 @@ extern "C" __global__ void __launch_bounds__(IMP_MEAN_BLOCK)
     const int ds = (int)(t / P.n_rows);
     ev += imp_mean_dispatch<0>(ds >> 1, P, r, ds & 1, smem + threadIdx.x, S);
   }
-  if (ev) atomicAdd((unsigned long long*)P.evals, ev);
+  if (ev) atomicAdd((unsigned long long*)P.evals + 5, ev);   // mean-range NM
 }
 
 // ---------------------------------------------------------------------------
