@@ -630,7 +630,15 @@ struct K5Shape {
 #ifndef IMP_K5_WCTA
 #define IMP_K5_WCTA 128
 #endif
-  static constexpr int W = TEAM > 32 ? IMP_K5_WCTA : IMP_K5_WWARP;
+// the 256 / 512-thread classes capture a twice wider window (room for it
+// in shared memory at their occupancy; vehicle3d 239 -> 256 phase-1
+// sweeps/s, dim14 541 -> 641; the 128-thread class would lose blocks per
+// SM: room5d 206 -> 190.  profiles/r02/k5_window_ab.txt)
+#ifndef IMP_K5_WCTA_BIG
+#define IMP_K5_WCTA_BIG 256
+#endif
+  static constexpr int W = TEAM > 32 ? (TEAM >= 256 ? IMP_K5_WCTA_BIG : IMP_K5_WCTA)
+                                     : IMP_K5_WWARP;
   static constexpr int WIN = 2 * 2 * W;   // [track][slot] {h, w}
 };
 
