@@ -628,14 +628,13 @@ struct K5Shape {
 #define IMP_K5_WWARP 32
 #endif
 #ifndef IMP_K5_WCTA
-#define IMP_K5_WCTA 128
+#define IMP_K5_WCTA 256
 #endif
-// the 256 / 512-thread classes capture a twice wider window (room for it
-// in shared memory at their occupancy; vehicle3d 239 -> 256 phase-1
-// sweeps/s, dim14 541 -> 641; the 128-thread class would lose blocks per
-// SM: room5d 206 -> 190.  profiles/r02/k5_window_ab.txt)
+// 256-rank windows for every CTA class (vehicle3d 239 -> 256 phase-1
+// sweeps/s, dim14 541 -> 641; the 128-thread class with a single buffer,
+// see IMP_K5_WSINGLE.  profiles/r02/k5_window_ab.txt)
 #ifndef IMP_K5_WCTA_BIG
-#define IMP_K5_WCTA_BIG 256
+#define IMP_K5_WCTA_BIG IMP_K5_WCTA
 #endif
   static constexpr int W = TEAM > 32 ? (TEAM >= 256 ? IMP_K5_WCTA_BIG : IMP_K5_WCTA)
                                      : IMP_K5_WWARP;
@@ -1101,6 +1100,13 @@ __device__ __forceinline__ bool walk_track(bool zero, bool known, double s,
 // CTA teams of <= IMP_K5_ENDSYNC threads end each row with a barrier
 // (room5d's 128-thread rows: 188 vs 183 phase-1 sweeps/s with it; the
 // 256 / 512 classes are faster without)
+// the 128-thread class ends rows with a barrier, so one window buffer
+// (cleared before it) suffices: half the shared memory, room for a 256-rank
+// window at the same occupancy (room5d 206 -> 215 phase-1 sweeps/s,
+// profiles/r02/k5_window_ab.txt)
+#ifndef IMP_K5_WSINGLE
+#define IMP_K5_WSINGLE 1
+#endif
 #ifndef IMP_K5_ENDSYNC
 #define IMP_K5_ENDSYNC 128
 #endif
@@ -1118,7 +1124,11 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
   __shared__ Fix x_part[4 * SH::NW];
   __shared__ unsigned long long hist_all[TEAMS_PER_BLOCK][SH::HIST];
   __shared__ SearchState s_st[TEAMS_PER_BLOCK];
-  __shared__ double2 s_win[TEAMS_PER_BLOCK][2][SH::WIN];   // row parity
+  // window buffers: two by row parity, or one for the classes that end a
+  // row with a barrier anyway (cleared before it)
+  constexpr bool SINGLE = IMP_K5_WSINGLE && TEAM <= IMP_K5_ENDSYNC;
+  constexpr int NBUF = SINGLE ? 1 : 2;
+  __shared__ double2 s_win[TEAMS_PER_BLOCK][NBUF][SH::WIN];
   __shared__ double s_lw[TEAMS_PER_BLOCK][2];
   __shared__ Fix s_x[TEAMS_PER_BLOCK][4];
   __shared__ int s_need[TEAMS_PER_BLOCK][2];
@@ -1134,7 +1144,7 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     if constexpr (TEAM == 32) __syncwarp();
     else __syncthreads();
   };
-  for (int q = tid; q < 2 * SH::WIN; q += TEAM)
+  for (int q = tid; q < NBUF * SH::WIN; q += TEAM)
     (&s_win[slot][0][0])[q] = make_double2(0.0, 0.0);
   team_sync();
 
@@ -1163,13 +1173,15 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     // ranked in [g - W, g + W) per track.  The window buffer is
     // double-buffered by row parity (cleared during the previous row's
     // reduction).
-    const int par = (int)((i / nteams) & 1);
+    const int par = SINGLE ? 0 : (int)((i / nteams) & 1);
     double2* win = s_win[slot][par];
     const int wb0 = g0 - W, wb1 = g1 - W;
     // clear the next row's window buffer: its last readers (the previous
     // row's walk) finished before the previous row's second barrier
-    for (int q = tid; q < 2 * SH::WIN; q += TEAM)
-      (&s_win[slot][par ^ 1][0].x)[q] = 0.0;
+    if constexpr (!SINGLE) {
+      for (int q = tid; q < 2 * SH::WIN; q += TEAM)
+        (&s_win[slot][par ^ 1][0].x)[q] = 0.0;
+    }
     double fv[2] = {0.0, 0.0};
     Fix xs[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};   // C0 F0 C1 F1
     for_slots<TEAM, WIDE>(a, tid, row, beg, m,
@@ -1300,6 +1312,9 @@ __global__ void __launch_bounds__(TEAM == 32 ? 256 : TEAM,
     // no barrier needed here: the next row writes s_st / s_x / s_need /
     // s_lw and the partials only after its first barrier, which thread 0
     // reaches once it is done with this row's
+    if constexpr (SINGLE) {   // the walks read the window before B2
+      for (int q = tid; q < 2 * SH::WIN; q += TEAM) (&win[0].x)[q] = 0.0;
+    }
     if constexpr (TEAM <= IMP_K5_ENDSYNC) __syncthreads();
   }
 }
